@@ -1,0 +1,365 @@
+"""Code construction feeding the GPU layout compiler.
+
+Mirrors the parts of the reference's ``qsagms.code`` (pkg/src/qsagms/code.py)
+that produce decoder inputs.  The Tanner-graph arrays are produced by the
+native layout compiler (``qsg_graph_create_gb`` / ``qsg_graph_create_csr``
+with device -1, i.e. host only) and exported in the reference's
+``TannerGraph`` layout (code.py:118-191), so a graph built here and a graph
+built by the reference are interchangeable inputs to ``decode_batch``.
+
+Also provides the seeded random-GB generator needed by BASELINE configs 3-5
+(not present in the reference) and QPC text I/O
+(code.py:279-378).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from functools import cached_property
+from pathlib import Path
+
+import numpy as np
+
+from . import _native
+
+
+@dataclass(frozen=True)
+class GbSpec:
+    """Circulant size and exponent sets of a GB code (code.py:48-65)."""
+
+    ell: int
+    a_exponents: tuple[int, ...]
+    b_exponents: tuple[int, ...]
+
+    def __post_init__(self):
+        if self.ell < 1:
+            raise ValueError("ell must be positive")
+        for name, exps in (("a", self.a_exponents), ("b", self.b_exponents)):
+            if not exps:
+                raise ValueError(f"{name} exponent set is empty")
+            if len(set(exps)) != len(exps):
+                raise ValueError(f"duplicate exponent in {name}")
+            if any(e < 0 or e >= self.ell for e in exps):
+                raise ValueError(f"{name} exponents must lie in [0, ell)")
+
+
+@dataclass(eq=False)
+class CodeGraph:
+    """Decoder-ready Tanner graph in the reference's TannerGraph layout.
+
+    Edges are numbered row-major (check, then column), which fixes every
+    reduction order of the decoder.  ``vn_order`` lists each qubit's edges
+    by ascending check index; ``vn_inverse`` is its inverse permutation.
+    """
+
+    n: int
+    m: int
+    edge_cn: np.ndarray = field(repr=False)
+    edge_vn: np.ndarray = field(repr=False)
+    edge_sym: np.ndarray = field(repr=False)
+    cn_ptr: np.ndarray = field(repr=False)
+    vn_order: np.ndarray = field(repr=False)
+    vn_ptr: np.ndarray = field(repr=False)
+    kind: int = 0
+    gb: GbSpec | None = None
+
+    @property
+    def edge_count(self) -> int:
+        return int(self.edge_cn.shape[0])
+
+    @cached_property
+    def vn_inverse(self) -> np.ndarray:
+        inv = np.empty(self.edge_count, dtype=np.int64)
+        inv[self.vn_order] = np.arange(self.edge_count, dtype=np.int64)
+        return inv
+
+    @cached_property
+    def cn_degrees(self) -> np.ndarray:
+        return np.diff(self.cn_ptr)
+
+    @cached_property
+    def vn_degrees(self) -> np.ndarray:
+        return np.diff(self.vn_ptr)
+
+    @cached_property
+    def edges(self) -> list[tuple[int, int, int]]:
+        return list(zip(self.edge_cn.tolist(), self.edge_vn.tolist(), self.edge_sym.tolist()))
+
+    @cached_property
+    def cn_adjacency(self) -> list[list[int]]:
+        return [list(range(self.cn_ptr[i], self.cn_ptr[i + 1])) for i in range(self.m)]
+
+    @cached_property
+    def vn_adjacency(self) -> list[list[int]]:
+        return [self.vn_order[self.vn_ptr[j]:self.vn_ptr[j + 1]].tolist() for j in range(self.n)]
+
+    @property
+    def rows(self) -> list[list[tuple[int, int]]]:
+        """Sparse rows [(column, symbol)] (SparseCheckMatrix.rows layout)."""
+        return [list(zip(self.edge_vn[a:b].tolist(), self.edge_sym[a:b].tolist()))
+                for a, b in zip(self.cn_ptr[:-1], self.cn_ptr[1:])]
+
+    def syndromes_of(self, e: np.ndarray) -> np.ndarray:
+        """Host-side syndrome of error patterns (B, n) -> (B, m); used to
+        re-verify reported successes (decoder.py:528-531), not on the hot path."""
+        e = np.atleast_2d(np.asarray(e, dtype=np.uint8))
+        c = e[:, self.edge_vn]
+        s = self.edge_sym
+        t = ((c & 1) & (s >> 1)) ^ ((c >> 1) & (s & 1))
+        return (np.add.reduceat(t.astype(np.int64), self.cn_ptr[:-1], axis=1) & 1).astype(np.uint8)
+
+
+def _export(handle, gb=None) -> CodeGraph:
+    L = _native.lib()
+    n, m, dcm, dvm, kind, thr = (C.c_int32() for _ in range(6))
+    E = C.c_int64()
+    _native.check(L.qsg_graph_info(handle, C.byref(n), C.byref(m), C.byref(E), C.byref(dcm),
+                                   C.byref(dvm), C.byref(kind), C.byref(thr)))
+    arrs = dict(
+        edge_cn=np.zeros(E.value, np.int64), edge_vn=np.zeros(E.value, np.int64),
+        edge_sym=np.zeros(E.value, np.uint8), cn_ptr=np.zeros(m.value + 1, np.int64),
+        vn_order=np.zeros(E.value, np.int64), vn_ptr=np.zeros(n.value + 1, np.int64),
+    )
+    _native.check(L.qsg_graph_export(handle, *(a.ctypes.data for a in arrs.values())))
+    return CodeGraph(n=n.value, m=m.value, kind=kind.value, gb=gb, **arrs)
+
+
+def _with_host_handle(create):
+    handle = C.c_void_p()
+    _native.check(create(C.byref(handle)))
+    return handle
+
+
+def gb_graph(spec: GbSpec) -> CodeGraph:
+    """tanner_graph(build_gb(spec)) via the native layout compiler
+    (code.py:150-231)."""
+    L = _native.lib()
+    a = np.ascontiguousarray(spec.a_exponents, dtype=np.int32)
+    b = np.ascontiguousarray(spec.b_exponents, dtype=np.int32)
+    h = _with_host_handle(lambda out: L.qsg_graph_create_gb(
+        spec.ell, a.ctypes.data, len(a), b.ctypes.data, len(b), -1, out))
+    try:
+        return _export(h, gb=spec)
+    finally:
+        L.qsg_graph_destroy(h)
+
+
+def csr_graph(n: int, rows) -> CodeGraph:
+    """Tanner graph of an arbitrary check matrix given as sparse rows
+    [(column, symbol)], columns strictly increasing (code.py:150-191)."""
+    L = _native.lib()
+    cn_ptr = np.zeros(len(rows) + 1, dtype=np.int64)
+    cols, syms = [], []
+    for i, row in enumerate(rows):
+        for j, s in row:
+            cols.append(int(j))
+            syms.append(int(s))
+        cn_ptr[i + 1] = len(cols)
+    ev = np.ascontiguousarray(cols, dtype=np.int64)
+    es = np.ascontiguousarray(syms, dtype=np.uint8)
+    h = _with_host_handle(lambda out: L.qsg_graph_create_csr(
+        int(n), len(rows), cn_ptr.ctypes.data, ev.ctypes.data, es.ctypes.data, -1, out))
+    try:
+        return _export(h)
+    finally:
+        L.qsg_graph_destroy(h)
+
+
+def as_code_graph(graph) -> CodeGraph:
+    """Accept this package's CodeGraph or any TannerGraph-like object (the
+    reference's ``qsagms.code.TannerGraph``)."""
+    if isinstance(graph, CodeGraph):
+        return graph
+    return CodeGraph(
+        n=int(graph.n), m=int(graph.m),
+        edge_cn=np.asarray(graph.edge_cn, dtype=np.int64),
+        edge_vn=np.asarray(graph.edge_vn, dtype=np.int64),
+        edge_sym=np.asarray(graph.edge_sym, dtype=np.uint8),
+        cn_ptr=np.asarray(graph.cn_ptr, dtype=np.int64),
+        vn_order=np.asarray(graph.vn_order, dtype=np.int64),
+        vn_ptr=np.asarray(graph.vn_ptr, dtype=np.int64),
+    )
+
+
+# -- code parameters -------------------------------------------------------------
+
+def gf2_rank_bits(rows: list[int]) -> int:
+    """GF(2) rank of bit-packed rows (Gaussian elimination on Python ints)."""
+    pivots: dict[int, int] = {}
+    rank = 0
+    for r in rows:
+        while r:
+            top = r.bit_length() - 1
+            if top not in pivots:
+                pivots[top] = r
+                rank += 1
+                break
+            r ^= pivots[top]
+    return rank
+
+
+def code_dimension(graph: CodeGraph) -> int:
+    """k = n - rank of the symplectic [X | Z] expansion (code.py:234-276)."""
+    packed = []
+    for a, b in zip(graph.cn_ptr[:-1], graph.cn_ptr[1:]):
+        bits = 0
+        for j, s in zip(graph.edge_vn[a:b].tolist(), graph.edge_sym[a:b].tolist()):
+            if s & 1:
+                bits |= 1 << j
+            if s >> 1:
+                bits |= 1 << (graph.n + j)
+        packed.append(bits)
+    return graph.n - gf2_rank_bits(packed)
+
+
+def gb_dimension(spec: GbSpec) -> int:
+    """k = 2 deg gcd(a(x), b(x), x^ell - 1) over GF(2) for GB codes."""
+    def pmod(a, b):
+        db = b.bit_length()
+        while a and a.bit_length() >= db:
+            a ^= b << (a.bit_length() - db)
+        return a
+
+    def pgcd(a, b):
+        while b:
+            a, b = b, pmod(a, b)
+        return a
+
+    a = sum(1 << e for e in spec.a_exponents)
+    b = sum(1 << e for e in spec.b_exponents)
+    g = pgcd(pgcd(a, b), (1 << spec.ell) | 1)
+    return 2 * (g.bit_length() - 1)
+
+
+def random_gb_spec(ell: int, w: int, seed: int, max_draws: int = 10_000) -> GbSpec:
+    """Seeded random GB code for BASELINE configs 3-5.
+
+    a(x) and b(x) each get w distinct exponents: 0 plus w-1 drawn uniformly
+    without replacement from [1, ell) by ``numpy.random.default_rng(seed)``;
+    a draw with k = 0 is rejected and redrawn from the same generator.  The
+    reference has no such generator; this rule is the
+    builder's definition and is pinned by tests/test_codes.py.
+    """
+    if w < 1 or w > ell:
+        raise ValueError("need 1 <= w <= ell")
+    rng = np.random.default_rng(seed)
+    for _ in range(max_draws):
+        a = (0,) + tuple(sorted(int(x) for x in rng.choice(np.arange(1, ell), size=w - 1, replace=False)))
+        b = (0,) + tuple(sorted(int(x) for x in rng.choice(np.arange(1, ell), size=w - 1, replace=False)))
+        spec = GbSpec(ell, a, b)
+        if gb_dimension(spec) > 0:
+            return spec
+    raise RuntimeError("no k > 0 code found")
+
+
+# -- QPC 1 text format (code.py:279-378) --------------------------------------------
+
+PAULI_NAMES = "IXZY"
+PAULI_CODES = {"I": 0, "X": 1, "Z": 2, "Y": 3}
+
+
+class CodeFormatError(ValueError):
+    """Malformed code file, with the 1-based line number when known."""
+
+    def __init__(self, message: str, line: int | None = None):
+        self.line = line
+        super().__init__((f"line {line}: " if line is not None else "") + message)
+
+
+def load_qpc(path) -> CodeGraph:
+    """Parse a QPC 1 file into a CodeGraph (validation errors carry line
+    numbers like code.py:292-378; commutation is checked by ``check_commute``)."""
+    lines = []
+    for num, raw in enumerate(Path(path).read_text(encoding="utf-8").splitlines(), start=1):
+        text = raw.split("#", 1)[0].strip()
+        if text:
+            lines.append((num, text))
+    if not lines:
+        raise CodeFormatError("empty file")
+    num, head = lines[0]
+    if head != "QPC 1":
+        raise CodeFormatError(f"expected 'QPC 1' header, got {head!r}", num)
+    if len(lines) < 2:
+        raise CodeFormatError("missing dimension line", num)
+    num, dims = lines[1]
+    try:
+        kv = dict(part.split("=", 1) for part in dims.split())
+        n, m = int(kv["n"]), int(kv["m"])
+    except (ValueError, KeyError):
+        raise CodeFormatError(f"expected 'n=<int> m=<int>', got {dims!r}", num) from None
+    if n < 1 or m < 1:
+        raise CodeFormatError("n and m must be positive", num)
+    body = lines[2:]
+    gb = None
+    if body and body[0][1].startswith("gb "):
+        num, text = body[0]
+        try:
+            kv = dict(part.split("=", 1) for part in text[3:].split())
+            gb = GbSpec(int(kv["ell"]), tuple(int(e) for e in kv["a"].split(",")),
+                        tuple(int(e) for e in kv["b"].split(",")))
+        except (ValueError, KeyError) as exc:
+            raise CodeFormatError(f"bad gb line: {exc}", num) from None
+        body = body[1:]
+    if len(body) != m:
+        raise CodeFormatError(f"expected {m} row lines, found {len(body)}",
+                              body[-1][0] if body else num)
+    rows = []
+    for want, (num, text) in enumerate(body):
+        idx, _, rest = text.partition(":")
+        try:
+            i = int(idx)
+        except ValueError:
+            raise CodeFormatError(f"expected row index, got {idx!r}", num) from None
+        if i != want:
+            raise CodeFormatError(f"row index {i} out of order (expected {want})", num)
+        row, prev = [], -1
+        for tok in rest.split():
+            c, _, s = tok.partition(":")
+            try:
+                j, sym = int(c), PAULI_CODES[s]
+            except (ValueError, KeyError):
+                raise CodeFormatError(f"bad entry {tok!r}", num) from None
+            if sym == 0:
+                raise CodeFormatError("identity symbol not allowed in a row", num)
+            if not 0 <= j < n:
+                raise CodeFormatError(f"column {j} outside [0, {n})", num)
+            if j <= prev:
+                raise CodeFormatError(f"columns must be strictly increasing (column {j})", num)
+            row.append((j, sym))
+            prev = j
+        rows.append(row)
+    g = csr_graph(n, rows)
+    g.gb = gb
+    return g
+
+
+def save_qpc(graph: CodeGraph, path) -> None:
+    """Write QPC 1 (LF newlines), code.py:279-289."""
+    out = ["QPC 1", f"n={graph.n} m={graph.m}"]
+    if graph.gb is not None:
+        out.append(f"gb ell={graph.gb.ell} a={','.join(map(str, graph.gb.a_exponents))} "
+                   f"b={','.join(map(str, graph.gb.b_exponents))}")
+    for i, row in enumerate(graph.rows):
+        out.append(f"{i}: " + " ".join(f"{j}:{PAULI_NAMES[s]}" for j, s in row))
+    Path(path).write_text("\n".join(out) + "\n", encoding="utf-8", newline="\n")
+
+
+def check_commute(graph: CodeGraph) -> bool:
+    """True iff all rows commute (symplectic inner products vanish)."""
+    cols = [dict(r) for r in graph.rows]
+    by_col: dict[int, list[int]] = {}
+    for i, r in enumerate(cols):
+        for j in r:
+            by_col.setdefault(j, []).append(i)
+    for i, r in enumerate(cols):
+        acc: dict[int, int] = {}
+        for j, s in r.items():
+            for k in by_col[j]:
+                if k > i:
+                    t = cols[k][j]
+                    acc[k] = acc.get(k, 0) ^ (((s & 1) & (t >> 1)) ^ ((s >> 1) & (t & 1)))
+        if any(acc.values()):
+            return False
+    return True
+

@@ -1,0 +1,580 @@
+// C ABI (include/qsg.h): Tanner-graph layout compiler, launch configuration
+// and the entry points that replace the reference's FER-loop unit.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/qsg.h"
+#include "qsg_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error = "ok";
+
+int fail(int code, const std::string &msg)
+{
+    g_last_error = msg;
+    return code;
+}
+
+#define QSG_CUDA(call)                                                                  \
+    do {                                                                                \
+        cudaError_t err_ = (call);                                                      \
+        if (err_ != cudaSuccess)                                                        \
+            return fail(QSG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(err_)); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev)
+    {
+        if (dev < 0) return;  // host-only graph: no CUDA calls at all
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard()
+    {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+int next_pow2(int x)
+{
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+template <typename T>
+int upload(T **dst, const std::vector<T> &src)
+{
+    QSG_CUDA(cudaMalloc((void **)dst, std::max<size_t>(src.size(), 1) * sizeof(T)));
+    if (!src.empty()) QSG_CUDA(cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return QSG_OK;
+}
+
+void free_device(qsg_graph *g)
+{
+    cudaFree(g->d_cn_slot); cudaFree(g->d_cn_sym); cudaFree(g->d_cn_deg);
+    cudaFree(g->d_vn_sym); cudaFree(g->d_vn_deg); cudaFree(g->d_slot_edge);
+    cudaFree(g->d_cn_ptr); cudaFree(g->d_edge_vn); cudaFree(g->d_edge_sym);
+}
+
+bool bicycle_w_supported(int w)
+{
+    for (int x : qsg::kBicycleWs)
+        if (x == w) return true;
+    return false;
+}
+
+// ---- layout compiler ---------------------------------------------------------
+// Input: canonical CSR (TannerGraph order, code.py:150-191).  Output: the
+// TannerGraph arrays (kept for export), the qubit-major slot layout
+// (slot = s * n_pad + j for the s-th edge of qubit j), the k-major check
+// slot table, and the kernel kind (generic or bicycle W).
+int compile_layout(qsg_graph *g, int32_t n, int32_t m, const int64_t *cn_ptr, const int64_t *edge_vn,
+                   const uint8_t *edge_sym)
+{
+    if (n < 1 || m < 1) return fail(QSG_EINVAL, "n and m must be positive");
+    if (!cn_ptr || !edge_vn || !edge_sym) return fail(QSG_EINVAL, "null CSR array");
+    if (cn_ptr[0] != 0) return fail(QSG_EINVAL, "cn_ptr[0] must be 0");
+    const int64_t E = cn_ptr[m];
+    if (E < 1) return fail(QSG_EINVAL, "graph has no edges");
+    g->n = n; g->m = m; g->E = E;
+    g->cn_ptr.assign(cn_ptr, cn_ptr + m + 1);
+    g->edge_vn.assign(edge_vn, edge_vn + E);
+    g->edge_sym.assign(edge_sym, edge_sym + E);
+    g->edge_cn.resize(E);
+    std::vector<int64_t> vdeg(n, 0);
+    int32_t dc_max = 0;
+    for (int i = 0; i < m; ++i) {
+        if (cn_ptr[i + 1] <= cn_ptr[i]) return fail(QSG_EINVAL, "graph has isolated checks");
+        dc_max = std::max<int32_t>(dc_max, (int32_t)(cn_ptr[i + 1] - cn_ptr[i]));
+        int64_t prev = -1;
+        for (int64_t e = cn_ptr[i]; e < cn_ptr[i + 1]; ++e) {
+            const int64_t j = edge_vn[e];
+            if (j < 0 || j >= n) return fail(QSG_EINVAL, "row " + std::to_string(i) + ": column out of range");
+            if (j <= prev) return fail(QSG_EINVAL, "row " + std::to_string(i) + ": columns not strictly increasing");
+            if (edge_sym[e] < 1 || edge_sym[e] > 3) return fail(QSG_EINVAL, "symbol is not a nonzero Pauli");
+            prev = j;
+            g->edge_cn[e] = i;
+            vdeg[j]++;
+        }
+    }
+    int32_t dv_max = 0;
+    g->vn_ptr.assign(n + 1, 0);
+    for (int j = 0; j < n; ++j) {
+        if (vdeg[j] == 0) return fail(QSG_EINVAL, "graph has isolated qubits");
+        dv_max = std::max<int32_t>(dv_max, (int32_t)vdeg[j]);
+        g->vn_ptr[j + 1] = g->vn_ptr[j] + vdeg[j];
+    }
+    // vn_order: edges of each qubit in ascending check (= canonical) order
+    g->vn_order.assign(E, 0);
+    std::vector<int64_t> fill(g->vn_ptr.begin(), g->vn_ptr.end() - 1);
+    std::vector<int32_t> pos_in_vn(E);
+    for (int64_t e = 0; e < E; ++e) {
+        const int64_t j = edge_vn[e];
+        pos_in_vn[e] = (int32_t)(fill[j] - g->vn_ptr[j]);
+        g->vn_order[fill[j]++] = e;
+    }
+    g->dc_max = dc_max;
+    g->dv_max = dv_max;
+    g->n_pad = next_pow2(std::max(n, 32));
+    g->log2_npad = 0;
+    while ((1 << g->log2_npad) < g->n_pad) ++g->log2_npad;
+    g->m_pad = (m + 31) / 32 * 32;
+
+    // kernel kind
+    int kind = 0;
+    if (dv_max % 2 == 0 && bicycle_w_supported(dv_max / 2) && (int64_t)dv_max * g->n_pad <= 32768) {
+        const int W = dv_max / 2;
+        bool ok = true;
+        for (int i = 0; i < m && ok; ++i) {
+            ok = (cn_ptr[i + 1] - cn_ptr[i]) == 2 * W;
+            for (int64_t e = cn_ptr[i]; e < cn_ptr[i + 1] && ok; ++e) ok = edge_sym[e] == edge_sym[cn_ptr[i]];
+            ok = ok && (edge_sym[cn_ptr[i]] == 1 || edge_sym[cn_ptr[i]] == 2);
+        }
+        for (int j = 0; j < n && ok; ++j) {
+            ok = vdeg[j] == 2 * W;
+            for (int s = 0; s < 2 * W && ok; ++s)
+                ok = edge_sym[g->vn_order[g->vn_ptr[j] + s]] == (s < W ? 1 : 2);
+        }
+        if (ok) kind = W;
+    }
+    g->kind = kind;
+    if (kind == 0) {
+        if (dc_max > qsg::kGenericMaxDeg || dv_max > qsg::kGenericMaxDeg)
+            return fail(QSG_EUNSUPPORTED, "node degree exceeds the generic kernel limit (32)");
+        if ((int64_t)dv_max * g->n_pad > 65535)
+            return fail(QSG_EUNSUPPORTED, "graph too large for 16-bit slot tables");
+    }
+    // threads per frame: every thread owns <= 32 checks (register bit masks)
+    const int nodes = std::max(n, m);
+    if (nodes <= 32 * 12) g->threads = 32;
+    else if (m <= 128 * 32) g->threads = 128;
+    else return fail(QSG_EUNSUPPORTED, "more than 4096 checks");
+
+    // check slot table, k-major [dc_max][m_pad]
+    const int mp = g->m_pad, np_ = g->n_pad;
+    std::vector<uint16_t> cn_slot((size_t)dc_max * mp, 0);
+    std::vector<uint8_t> cn_sym((size_t)dc_max * mp, 0), cn_deg(mp, 0);
+    std::vector<uint8_t> vn_sym((size_t)dv_max * np_, 0), vn_deg(np_, 0);
+    std::vector<int32_t> slot_edge((size_t)dv_max * np_, -1);
+    for (int i = 0; i < m; ++i) {
+        cn_deg[i] = (uint8_t)(cn_ptr[i + 1] - cn_ptr[i]);
+        for (int64_t e = cn_ptr[i]; e < cn_ptr[i + 1]; ++e) {
+            const int k = (int)(e - cn_ptr[i]);
+            const uint32_t slot = (uint32_t)pos_in_vn[e] * np_ + (uint32_t)edge_vn[e];
+            uint32_t ent = slot;
+            if (kind > 0 && edge_sym[e] == 1) ent |= 0x8000u;
+            cn_slot[(size_t)k * mp + i] = (uint16_t)ent;
+            cn_sym[(size_t)k * mp + i] = edge_sym[e];
+            slot_edge[slot] = (int32_t)e;
+        }
+    }
+    for (int j = 0; j < n; ++j) {
+        vn_deg[j] = (uint8_t)vdeg[j];
+        for (int64_t q = g->vn_ptr[j]; q < g->vn_ptr[j + 1]; ++q)
+            vn_sym[(size_t)(q - g->vn_ptr[j]) * np_ + j] = edge_sym[g->vn_order[q]];
+    }
+    if (g->device < 0) {
+        g->tab_bytes = g->group_bytes = 0;
+        return QSG_OK;
+    }
+    int rc;
+    if ((rc = upload(&g->d_cn_slot, cn_slot)) || (rc = upload(&g->d_slot_edge, slot_edge))) return rc;
+    if (kind == 0) {
+        if ((rc = upload(&g->d_cn_sym, cn_sym)) || (rc = upload(&g->d_cn_deg, cn_deg)) ||
+            (rc = upload(&g->d_vn_sym, vn_sym)) || (rc = upload(&g->d_vn_deg, vn_deg)))
+            return rc;
+    }
+    std::vector<int32_t> cp32(g->cn_ptr.begin(), g->cn_ptr.end()), ev32(g->edge_vn.begin(), g->edge_vn.end());
+    if ((rc = upload(&g->d_cn_ptr, cp32)) || (rc = upload(&g->d_edge_vn, ev32)) ||
+        (rc = upload(&g->d_edge_sym, g->edge_sym)))
+        return rc;
+
+    // shared-memory footprint
+    size_t tab = (size_t)dc_max * mp * 2;
+    if (kind == 0) tab += (size_t)dc_max * mp + mp + (size_t)dv_max * np_ + np_;
+    g->tab_bytes = (uint32_t)((tab + 15) / 16 * 16);
+    const int T = g->threads;
+    size_t grp = (size_t)dv_max * np_ * 4 + np_ + 2 * (T / 32) * 4 + 8;
+    g->group_bytes = (uint32_t)((grp + 15) / 16 * 16);
+    return QSG_OK;
+}
+
+int validate_cfg(const qsg_decoder_cfg *c)
+{
+    if (!c) return fail(QSG_EINVAL, "null decoder config");
+    if (c->variant < QSG_BP4 || c->variant > QSG_SAGMS) return fail(QSG_EINVAL, "unknown variant");
+    if (c->vn_mode != QSG_VN_MARGINAL && c->vn_mode != QSG_VN_ADDITIVE) return fail(QSG_EINVAL, "unknown vn_mode");
+    if (c->l_max < 1) return fail(QSG_EINVAL, "l_max must be at least 1");
+    if (c->variant == QSG_SMS && !(c->alpha > 0.0 && c->alpha <= 1.0))
+        return fail(QSG_EINVAL, "sms requires alpha in (0, 1]");
+    if (c->variant == QSG_SAGMS) {  // GainParams.__post_init__, decoder.py:75-88
+        if (!(0.0 < c->alpha_min && c->alpha_min <= c->alpha_max && c->alpha_max <= 1.0))
+            return fail(QSG_EINVAL, "need 0 < alpha_min <= alpha_max <= 1");
+        if (!(c->eta_unsat >= 1.0)) return fail(QSG_EINVAL, "eta_unsat must be >= 1");
+        if (c->alpha_max * c->eta_unsat > 1.0) return fail(QSG_EINVAL, "stability constraint alpha_max*eta_unsat <= 1 violated");
+    }
+    return QSG_OK;
+}
+
+// u >= t  <=>  (w >> 11) >= ceil(t * 2^53)  (channel.py:70-75, exact).
+void thresholds(double eps, uint64_t K[3])
+{
+    const double t_x = 1.0 - eps, t_y = 1.0 - eps + eps / 3.0, t_z = 1.0 - eps / 3.0;
+    K[0] = (uint64_t)std::ceil(t_x * 9007199254740992.0);
+    K[1] = (uint64_t)std::ceil(t_y * 9007199254740992.0);
+    K[2] = (uint64_t)std::ceil(t_z * 9007199254740992.0);
+}
+
+// Pick groups-per-CTA maximising resident frames per SM for one kernel.
+int launch_cfg(qsg_graph *g, bool bp4, bool add, void *fn, qsg::LaunchCfg *out)
+{
+    std::lock_guard<std::mutex> lock(g->mu);
+    qsg::LaunchCfg &c = g->cfg_cache[bp4][add];
+    if (c.ok) { *out = c; return QSG_OK; }
+    int max_smem = 0;
+    QSG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
+    const int T = g->threads;
+    const int gmax = T == 32 ? 16 : 8;
+    qsg::LaunchCfg best;
+    for (int G = 1; G <= gmax; ++G) {
+        const size_t smem = g->tab_bytes + (size_t)G * g->group_bytes;
+        if (smem > (size_t)max_smem) break;
+        QSG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int nb = 0;
+        QSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, G * T, smem));
+        if (nb * G > best.ctas_per_sm * best.groups) {
+            best.groups = G; best.ctas_per_sm = nb; best.smem = smem; best.ok = nb > 0;
+        }
+    }
+    if (!best.ok) return fail(QSG_EUNSUPPORTED, "graph does not fit in shared memory");
+    QSG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)best.smem));
+    c = best;
+    *out = best;
+    return QSG_OK;
+}
+
+int launch_decode(qsg_graph *g, const qsg_decoder_cfg *cfg, qsg::KParams &p, cudaStream_t st)
+{
+    const bool bp4 = cfg->variant == QSG_BP4, add = cfg->vn_mode == QSG_VN_ADDITIVE;
+    void *fn = qsg::kernel_ptr(g->kind, g->threads, bp4, add);
+    if (!fn) return fail(QSG_EUNSUPPORTED, "no kernel for this graph kind");
+    qsg::LaunchCfg lc;
+    int rc = launch_cfg(g, bp4, add, fn, &lc);
+    if (rc) return rc;
+    if (p.count == 0) return QSG_OK;
+    const int64_t want = (p.count + lc.groups - 1) / lc.groups;
+    const int grid = (int)std::min<int64_t>(want, (int64_t)lc.ctas_per_sm * g->num_sms);
+    unsigned long long *queue = nullptr;
+    QSG_CUDA(cudaMallocAsync((void **)&queue, sizeof(unsigned long long), st));
+    QSG_CUDA(cudaMemsetAsync(queue, 0, sizeof(unsigned long long), st));
+    p.queue = queue;
+    p.groups = lc.groups;
+    void *args[] = {&p};
+    cudaError_t err = cudaLaunchKernel(fn, dim3(grid), dim3(lc.groups * g->threads), args, lc.smem, st);
+    cudaFreeAsync(queue, st);
+    if (err != cudaSuccess) return fail(QSG_ECUDA, std::string("decode launch: ") + cudaGetErrorString(err));
+    return QSG_OK;
+}
+
+void fill_graph_params(const qsg_graph *g, qsg::KParams &p)
+{
+    p.cn_slot = g->d_cn_slot; p.cn_sym = g->d_cn_sym; p.cn_deg = g->d_cn_deg;
+    p.vn_sym = g->d_vn_sym; p.vn_deg = g->d_vn_deg; p.slot_edge = g->d_slot_edge;
+    p.n = g->n; p.m = g->m; p.n_pad = g->n_pad; p.log2_npad = g->log2_npad; p.m_pad = g->m_pad;
+    p.dc_max = g->dc_max; p.dv_max = g->dv_max; p.E = g->E;
+    p.tab_bytes = g->tab_bytes; p.group_bytes = g->group_bytes;
+}
+
+void fill_cfg_params(const qsg_decoder_cfg *c, double l0, qsg::KParams &p)
+{
+    p.gain_mode = c->variant == QSG_SMS ? 1 : (c->variant == QSG_SAGMS ? 2 : 0);
+    p.l_max = c->l_max;
+    p.early_stop = c->early_stop ? 1 : 0;
+    p.l0 = (float)l0;
+    // decoder.py:405-406 (marginal init :255-261), double then one rounding
+    double v0 = c->vn_mode == QSG_VN_MARGINAL ? std::log1p(std::exp(-l0)) + l0 - 0.6931471805599453 : l0;
+    v0 = std::min(64.0, std::max(-64.0, v0));
+    p.v0 = (float)v0;
+    p.alpha = (float)c->alpha;
+    p.amin = c->alpha_min; p.amax = c->alpha_max; p.eta = c->eta_unsat;
+}
+
+// ---- standalone sampling / syndrome kernels ----------------------------------
+__global__ void sample_kernel(int32_t n, uint64_t seed, int64_t start, int64_t count, uint64_t kx,
+                              uint64_t ky, uint64_t kz, uint8_t *out)
+{
+    const int nblk = (n + 3) >> 2;
+    const int64_t total = count * nblk;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t f = t / nblk;
+        const int b = (int)(t - f * nblk);
+        const qsg::U64x4 w = qsg::philox4x64_10((uint64_t)b + 1, seed, (uint64_t)(start + f));
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (4 * b + q < n) out[f * n + 4 * b + q] = qsg::pauli_from_word(w.v[q], kx, ky, kz);
+    }
+}
+
+__global__ void syndrome_kernel(int32_t n, int32_t m, const int32_t *cn_ptr, const int32_t *edge_vn,
+                                const uint8_t *edge_sym, const uint8_t *e, int64_t B, uint8_t *syn)
+{
+    const int64_t total = B * m;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = t / m;
+        const int i = (int)(t - b * m);
+        uint32_t x = 0;
+        for (int k = cn_ptr[i]; k < cn_ptr[i + 1]; ++k) {
+            const uint32_t c = e[b * n + edge_vn[k]], s = edge_sym[k];
+            x ^= ((c & 1u) & (s >> 1)) ^ ((c >> 1) & (s & 1u));
+        }
+        syn[t] = (uint8_t)x;
+    }
+}
+
+int create_common(int32_t device, qsg_graph **out, qsg_graph **g)
+{
+    if (!out) return fail(QSG_EINVAL, "null output handle");
+    *out = nullptr;
+    if (device >= 0) {  // device -1: host-only layout (export/inspection, no decode)
+        int ndev = 0;
+        QSG_CUDA(cudaGetDeviceCount(&ndev));
+        if (device >= ndev) return fail(QSG_EINVAL, "invalid device ordinal");
+    } else if (device != -1) {
+        return fail(QSG_EINVAL, "invalid device ordinal");
+    }
+    *g = new (std::nothrow) qsg_graph();
+    if (!*g) return fail(QSG_ENOMEM, "host allocation failed");
+    (*g)->device = device;
+    if (device >= 0) {
+        cudaError_t err = cudaDeviceGetAttribute(&(*g)->num_sms, cudaDevAttrMultiProcessorCount, device);
+        if (err != cudaSuccess) {
+            delete *g;
+            return fail(QSG_ECUDA, std::string("cudaDeviceGetAttribute: ") + cudaGetErrorString(err));
+        }
+    }
+    return QSG_OK;
+}
+
+}  // namespace
+
+namespace qsg {
+void *kernel_ptr(int W, int T, bool bp4, bool additive)
+{
+    switch (W) {
+    case 0: return kernel_ptr_w0(T, bp4, additive);
+    case 2: return kernel_ptr_w2(T, bp4, additive);
+    case 3: return kernel_ptr_w3(T, bp4, additive);
+    case 4: return kernel_ptr_w4(T, bp4, additive);
+    case 5: return kernel_ptr_w5(T, bp4, additive);
+    case 6: return kernel_ptr_w6(T, bp4, additive);
+    case 8: return kernel_ptr_w8(T, bp4, additive);
+    default: return nullptr;
+    }
+}
+}  // namespace qsg
+
+extern "C" {
+
+int qsg_abi_version(void) { return QSG_ABI_VERSION; }
+
+const char *qsg_last_error(void) { return g_last_error.c_str(); }
+
+int qsg_graph_create_csr(int32_t n, int32_t m, const int64_t *cn_ptr, const int64_t *edge_vn,
+                         const uint8_t *edge_sym, int32_t device, qsg_graph **out)
+{
+    qsg_graph *g = nullptr;
+    int rc = create_common(device, out, &g);
+    if (rc) return rc;
+    DeviceGuard dg(device);
+    rc = compile_layout(g, n, m, cn_ptr, edge_vn, edge_sym);
+    if (rc) {
+        if (device >= 0) free_device(g);
+        delete g;
+        return rc;
+    }
+    *out = g;
+    return QSG_OK;
+}
+
+int qsg_graph_create_gb(int32_t ell, const int32_t *a, int32_t wa, const int32_t *b, int32_t wb,
+                        int32_t device, qsg_graph **out)
+{
+    if (ell < 1) return fail(QSG_EINVAL, "ell must be positive");
+    if (!a || !b || wa < 1 || wb < 1) return fail(QSG_EINVAL, "exponent set is empty");
+    for (int pass = 0; pass < 2; ++pass) {  // GbSpec.__post_init__, code.py:56-65
+        const int32_t *x = pass ? b : a;
+        const int32_t w = pass ? wb : wa;
+        for (int i = 0; i < w; ++i) {
+            if (x[i] < 0 || x[i] >= ell) return fail(QSG_EINVAL, "exponents must lie in [0, ell)");
+            for (int k = 0; k < i; ++k)
+                if (x[k] == x[i]) return fail(QSG_EINVAL, "duplicate exponent");
+        }
+    }
+    // build_gb (code.py:201-231): sorted circulant supports per row
+    auto circ = [&](const int32_t *x, int w, int row, int sign) {
+        std::vector<int64_t> cols(w);
+        for (int k = 0; k < w; ++k) cols[k] = (((int64_t)row + sign * (int64_t)x[k]) % ell + ell) % ell;
+        std::sort(cols.begin(), cols.end());
+        return cols;
+    };
+    const int32_t m = 2 * ell, n = 2 * ell;
+    std::vector<int64_t> cn_ptr(1, 0), edge_vn;
+    std::vector<uint8_t> edge_sym;
+    for (int i = 0; i < ell; ++i) {
+        for (int64_t c : circ(a, wa, i, 1)) { edge_vn.push_back(c); edge_sym.push_back(1); }
+        for (int64_t c : circ(b, wb, i, 1)) { edge_vn.push_back(ell + c); edge_sym.push_back(1); }
+        cn_ptr.push_back((int64_t)edge_vn.size());
+    }
+    for (int i = 0; i < ell; ++i) {
+        for (int64_t c : circ(b, wb, i, -1)) { edge_vn.push_back(c); edge_sym.push_back(2); }
+        for (int64_t c : circ(a, wa, i, -1)) { edge_vn.push_back(ell + c); edge_sym.push_back(2); }
+        cn_ptr.push_back((int64_t)edge_vn.size());
+    }
+    return qsg_graph_create_csr(n, m, cn_ptr.data(), edge_vn.data(), edge_sym.data(), device, out);
+}
+
+int qsg_graph_destroy(qsg_graph *g)
+{
+    if (!g) return QSG_OK;
+    if (g->device >= 0) {
+        DeviceGuard dg(g->device);
+        free_device(g);
+    }
+    delete g;
+    return QSG_OK;
+}
+
+int qsg_graph_info(const qsg_graph *g, int32_t *n, int32_t *m, int64_t *E, int32_t *dc_max,
+                   int32_t *dv_max, int32_t *kind, int32_t *threads)
+{
+    if (!g) return fail(QSG_EINVAL, "null graph");
+    if (n) *n = g->n;
+    if (m) *m = g->m;
+    if (E) *E = g->E;
+    if (dc_max) *dc_max = g->dc_max;
+    if (dv_max) *dv_max = g->dv_max;
+    if (kind) *kind = g->kind;
+    if (threads) *threads = g->threads;
+    return QSG_OK;
+}
+
+int qsg_graph_export(const qsg_graph *g, int64_t *edge_cn, int64_t *edge_vn, uint8_t *edge_sym,
+                     int64_t *cn_ptr, int64_t *vn_order, int64_t *vn_ptr)
+{
+    if (!g) return fail(QSG_EINVAL, "null graph");
+    auto cp = [](auto *dst, const auto &v) {
+        if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+    };
+    cp(edge_cn, g->edge_cn); cp(edge_vn, g->edge_vn); cp(edge_sym, g->edge_sym);
+    cp(cn_ptr, g->cn_ptr); cp(vn_order, g->vn_order); cp(vn_ptr, g->vn_ptr);
+    return QSG_OK;
+}
+
+int qsg_decode_syndromes(const qsg_graph *gc, const qsg_decoder_cfg *cfg, double l0,
+                         const uint8_t *syndromes_dev, int64_t B, uint8_t *success_dev,
+                         uint8_t *e_hat_dev, int64_t *iterations_dev, const qsg_trace *trace,
+                         void *stream)
+{
+    qsg_graph *g = const_cast<qsg_graph *>(gc);
+    if (!g) return fail(QSG_EINVAL, "null graph");
+    if (g->device < 0) return fail(QSG_EINVAL, "graph was created host-only (device -1)");
+    int rc = validate_cfg(cfg);
+    if (rc) return rc;
+    if (B < 0) return fail(QSG_EINVAL, "negative batch size");
+    if (B > 0 && (!syndromes_dev || !success_dev || !iterations_dev)) return fail(QSG_EINVAL, "null buffer");
+    if (!std::isfinite(l0)) return fail(QSG_EINVAL, "prior llr must be finite");
+    DeviceGuard dg(g->device);
+    qsg::KParams p{};
+    fill_graph_params(g, p);
+    fill_cfg_params(cfg, l0, p);
+    p.sample = 0;
+    p.syn_in = syndromes_dev;
+    p.count = B;
+    p.out_flag = success_dev;
+    p.out_iters = iterations_dev;
+    p.out_ehat = e_hat_dev;
+    if (trace) {
+        p.tr_unsat = trace->unsat; p.tr_vn = trace->vn_msgs; p.tr_cn = trace->cn_msgs;
+        p.tr_counts = trace->counts;
+    }
+    return launch_decode(g, cfg, p, (cudaStream_t)stream);
+}
+
+int qsg_decode_frames(const qsg_graph *gc, const qsg_decoder_cfg *cfg, double epsilon, double epsilon0,
+                      uint64_t seed, int64_t start, int64_t count, uint8_t *fails_dev,
+                      int64_t *iterations_dev, uint8_t *e_hat_dev, int64_t *counters_dev, void *stream)
+{
+    qsg_graph *g = const_cast<qsg_graph *>(gc);
+    if (!g) return fail(QSG_EINVAL, "null graph");
+    if (g->device < 0) return fail(QSG_EINVAL, "graph was created host-only (device -1)");
+    int rc = validate_cfg(cfg);
+    if (rc) return rc;
+    if (!(epsilon >= 0.0 && epsilon < 1.0)) return fail(QSG_EINVAL, "epsilon must lie in [0, 1)");
+    if (!(epsilon0 > 0.0 && epsilon0 < 1.0)) return fail(QSG_EINVAL, "epsilon0 must lie in (0, 1)");
+    if (count < 0 || start < 0) return fail(QSG_EINVAL, "negative frame range");
+    DeviceGuard dg(g->device);
+    qsg::KParams p{};
+    fill_graph_params(g, p);
+    // prior_llr, channel.py:48-52
+    fill_cfg_params(cfg, std::log(3.0 * (1.0 - epsilon0) / epsilon0), p);
+    p.sample = 1;
+    p.seed = seed;
+    p.start = start;
+    uint64_t K[3];
+    thresholds(epsilon, K);
+    p.kx = K[0]; p.ky = K[1]; p.kz = K[2];
+    p.count = count;
+    p.out_flag = fails_dev;
+    p.out_iters = iterations_dev;
+    p.out_ehat = e_hat_dev;
+    p.counters = counters_dev;
+    return launch_decode(g, cfg, p, (cudaStream_t)stream);
+}
+
+int qsg_sample_errors(int32_t n, double epsilon, uint64_t seed, int64_t start, int64_t count,
+                      uint8_t *errors_dev, int32_t device, void *stream)
+{
+    if (n < 1) return fail(QSG_EINVAL, "n must be at least 1");
+    if (!(epsilon >= 0.0 && epsilon < 1.0)) return fail(QSG_EINVAL, "epsilon must lie in [0, 1)");
+    if (count < 0 || start < 0) return fail(QSG_EINVAL, "negative frame range");
+    if (count == 0) return QSG_OK;
+    if (!errors_dev) return fail(QSG_EINVAL, "null buffer");
+    DeviceGuard dg(device);
+    uint64_t K[3];
+    thresholds(epsilon, K);
+    const int64_t total = count * ((n + 3) / 4);
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
+    sample_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(n, seed, start, count, K[0], K[1], K[2], errors_dev);
+    QSG_CUDA(cudaGetLastError());
+    return QSG_OK;
+}
+
+int qsg_syndromes_of(const qsg_graph *g, const uint8_t *e_dev, int64_t B, uint8_t *syn_dev, void *stream)
+{
+    if (!g) return fail(QSG_EINVAL, "null graph");
+    if (g->device < 0) return fail(QSG_EINVAL, "graph was created host-only (device -1)");
+    if (B < 0) return fail(QSG_EINVAL, "negative batch size");
+    if (B == 0) return QSG_OK;
+    if (!e_dev || !syn_dev) return fail(QSG_EINVAL, "null buffer");
+    DeviceGuard dg(g->device);
+    const int64_t total = B * g->m;
+    const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
+    syndrome_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(g->n, g->m, g->d_cn_ptr, g->d_edge_vn,
+                                                            g->d_edge_sym, e_dev, B, syn_dev);
+    QSG_CUDA(cudaGetLastError());
+    return QSG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,60 @@
+// Internal declarations shared by the C-ABI translation unit and the kernel
+// instantiation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "qsg_kernel.cuh"
+
+namespace qsg {
+
+// Kernel envelope compiled into the library.
+constexpr int kBicycleWs[] = {2, 3, 4, 5, 6, 8};
+constexpr int kThreadCounts[] = {32, 128};
+
+// Returns the __global__ function for (W, T, bp4, additive) or nullptr.
+void *kernel_ptr(int W, int T, bool bp4, bool additive);
+void *kernel_ptr_w0(int T, bool bp4, bool additive);
+void *kernel_ptr_w2(int T, bool bp4, bool additive);
+void *kernel_ptr_w3(int T, bool bp4, bool additive);
+void *kernel_ptr_w4(int T, bool bp4, bool additive);
+void *kernel_ptr_w5(int T, bool bp4, bool additive);
+void *kernel_ptr_w6(int T, bool bp4, bool additive);
+void *kernel_ptr_w8(int T, bool bp4, bool additive);
+
+struct LaunchCfg {
+    int groups = 0;        // groups (frames in flight) per CTA
+    int ctas_per_sm = 0;
+    size_t smem = 0;
+    bool ok = false;
+};
+
+}  // namespace qsg
+
+// The opaque handle of include/qsg.h.
+struct qsg_graph {
+    int device = 0;
+    int32_t n = 0, m = 0;
+    int64_t E = 0;
+    int32_t dc_max = 0, dv_max = 0, kind = 0, threads = 32;
+    int32_t n_pad = 0, log2_npad = 0, m_pad = 0;
+    int32_t num_sms = 0;
+    // canonical TannerGraph arrays (host)
+    std::vector<int64_t> edge_cn, edge_vn, cn_ptr, vn_order, vn_ptr;
+    std::vector<uint8_t> edge_sym;
+    // device tables
+    uint16_t *d_cn_slot = nullptr;
+    uint8_t *d_cn_sym = nullptr, *d_cn_deg = nullptr, *d_vn_sym = nullptr, *d_vn_deg = nullptr;
+    int32_t *d_slot_edge = nullptr;
+    int32_t *d_cn_ptr = nullptr, *d_edge_vn = nullptr;
+    uint8_t *d_edge_sym = nullptr;
+    uint32_t tab_bytes = 0, group_bytes = 0;
+    // launch configurations cached per kernel instance
+    std::mutex mu;
+    qsg::LaunchCfg cfg_cache[2][2];  // [bp4][additive]
+};

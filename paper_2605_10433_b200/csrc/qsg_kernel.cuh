@@ -1,0 +1,559 @@
+// Persistent fused decode kernel for sm_100a.
+//
+// One "group" of T threads owns one frame at a time; a CTA holds G groups and
+// every group pulls frame indices from a global atomic queue until the batch
+// is exhausted (load balance across frames that stop after 2 or after 100
+// iterations).  Per frame the group runs, entirely in shared memory:
+//
+//   sample (Philox, channel.py:55-76) -> syndrome (decoder.py:303-309) ->
+//   for ell = 1..l_max (decoder.py:422-469):
+//     R: residual = syndrome ^ synd(e_hat), unsat via popc + group reduce
+//     exit on success / l_max; SAGMS gains from gamma (decoder.py:462-467)
+//     C: check-node update (min1/min2/sign or BP4 phi), decoder.py:311-338
+//     V: qubit-node update (marginal or additive), decoder.py:340-359, which
+//        also produces the next iteration's hard decision (the reduceat sums
+//        of hard_decisions, decoder.py:292-301, are the same sums).
+//
+// Message storage: ONE fp32 word per edge, updated in place (each edge is
+// owned by exactly one check and one qubit, and the C and V phases are
+// separated by group barriers).  Slot of the s-th edge of qubit j (qubit
+// order = ascending check index, code.py:171) is s * n_pad + j, so qubit
+// reads/writes are unit-stride across the group (conflict-free) and check
+// reads go through a per-graph u16 slot table (k-major, also conflict-free
+// for circulant codes).  Canonical edge order only matters for the BP4 phi
+// sum; the table lists each check's edges in canonical order.
+//
+// W > 0 selects the "bicycle" specialisation (all degrees 2W, each qubit's
+// edges X-then-Z, single-symbol checks: every GB code with |a| = |b| = W),
+// in which degrees, masks and numpy's pairwise summation tree are compile
+// time constants.  W == 0 is the generic table-driven path (any graph).
+#pragma once
+
+#include <stdint.h>
+
+#include "qsg_math.cuh"
+#include "qsg_philox.cuh"
+
+namespace qsg {
+
+constexpr int kGenericMaxDeg = 32;
+
+struct KParams {
+    // graph tables (global; copied to shared memory per CTA)
+    const uint16_t *cn_slot;   // [dc_max][m_pad]
+    const uint8_t *cn_sym;     // [dc_max][m_pad] generic only
+    const uint8_t *cn_deg;     // [m_pad]         generic only
+    const uint8_t *vn_sym;     // [dv_max][n_pad] generic only
+    const uint8_t *vn_deg;     // [n_pad]         generic only
+    const int32_t *slot_edge;  // [dv_max*n_pad]  canonical edge per slot (traces)
+    int32_t n, m, n_pad, log2_npad, m_pad, dc_max, dv_max;
+    int64_t E;
+    // decoder
+    int32_t gain_mode;  // 0: none (bp4/ms), 1: constant alpha (sms), 2: sagms
+    int32_t l_max, early_stop;
+    float l0, v0, alpha;
+    double amin, amax, eta;
+    // input
+    int32_t sample;  // 1: sample frames on device; 0: read syndromes
+    uint64_t seed;
+    int64_t start;
+    uint64_t kx, ky, kz;
+    const uint8_t *syn_in;
+    int64_t count;
+    // outputs
+    uint8_t *out_flag;  // fails (sample) or success (syndromes)
+    int64_t *out_iters;
+    uint8_t *out_ehat;
+    int64_t *counters;
+    unsigned long long *queue;
+    // traces (syndrome mode)
+    int32_t *tr_unsat;
+    float *tr_vn, *tr_cn;
+    int32_t *tr_counts;
+    // layout
+    int32_t groups;  // groups per CTA
+    uint32_t tab_bytes, group_bytes, syn_words;
+};
+
+// ---- optional-value arithmetic for compile-time masked reductions ---------
+// np.add.reduceat over cv * anti_mask keeps the masked (+-0) entries in
+// their tree positions; x + (+-0) == x, so dropping them from the tree is
+// value-identical.  With compile-time presence flags the dead adds vanish.
+struct OptF {
+    float v;
+    bool p;
+};
+__device__ __forceinline__ OptF oadd(OptF a, OptF b)
+{
+    if (!a.p) return b;
+    if (!b.p) return a;
+    return OptF{a.v + b.v, true};
+}
+
+// numpy pairwise_sum over a[0..N-1] (loops_utils.h.src), N <= 128.
+template <int N>
+__device__ __forceinline__ OptF pairwise_c(const OptF *a)
+{
+    if constexpr (N < 8) {
+        OptF r{0.0f, false};
+#pragma unroll
+        for (int i = 0; i < N; ++i) r = oadd(r, a[i]);
+        return r;
+    } else {
+        static_assert(N <= 128, "degree too large");
+        OptF r[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) r[k] = a[k];
+        constexpr int lim = N - (N % 8);
+#pragma unroll
+        for (int i = 8; i < lim; i += 8)
+#pragma unroll
+            for (int k = 0; k < 8; ++k) r[k] = oadd(r[k], a[i + k]);
+        OptF res = oadd(oadd(oadd(r[0], r[1]), oadd(r[2], r[3])),
+                        oadd(oadd(r[4], r[5]), oadd(r[6], r[7])));
+#pragma unroll
+        for (int i = lim; i < N; ++i) res = oadd(res, a[i]);
+        return res;
+    }
+}
+
+// One reduceat segment: x0 + pairwise(x1..x_{N-1}).  Absent total -> 0.
+template <int N>
+__device__ __forceinline__ float segsum_c(const OptF *a)
+{
+    const OptF r = oadd(a[0], pairwise_c<N - 1>(a + 1));
+    return r.p ? r.v : 0.0f;
+}
+
+// Runtime-length version for the generic path (masked entries are zeros).
+__device__ __forceinline__ float pairwise_rt(const float *a, int n)
+{
+    if (n < 8) {
+        float res = -0.0f;
+        for (int i = 0; i < n; ++i) res += a[i];
+        return res;
+    }
+    float r[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) r[k] = a[k];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) r[k] += a[i + k];
+    float res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += a[i];
+    return res;
+}
+__device__ __forceinline__ float segsum_rt(const float *a, int n) { return a[0] + pairwise_rt(a + 1, n - 1); }
+
+// argmin over (0, mX, mZ, mY) with ties to the lowest code (np.argmin,
+// decoder.py:301).
+__device__ __forceinline__ uint32_t hard_decision(float mX, float mZ, float mY)
+{
+    float best = 0.0f;
+    uint32_t e = 0;
+    if (mX < best) { best = mX; e = 1; }
+    if (mZ < best) { best = mZ; e = 2; }
+    if (mY < best) { e = 3; }
+    return e;
+}
+
+// ---- group synchronisation ---------------------------------------------
+template <int T>
+__device__ __forceinline__ void group_sync(int g)
+{
+    if constexpr (T == 32) {
+        __syncwarp();
+    } else {
+        asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(T) : "memory");
+    }
+}
+
+template <int T>
+__device__ __forceinline__ int group_sum(int v, int *scratch, int parity, int tid, int g)
+{
+    v = __reduce_add_sync(0xffffffffu, v);
+    if constexpr (T == 32) {
+        return v;
+    } else {
+        int *slot = scratch + parity * (T / 32);
+        if ((tid & 31) == 0) slot[tid >> 5] = v;
+        group_sync<T>(g);
+        int s = 0;
+#pragma unroll
+        for (int w = 0; w < T / 32; ++w) s += slot[w];
+        return s;
+    }
+}
+
+// Residual (or syndrome) bits of this thread's checks; bit t <-> check
+// tid + t*T.  e[] holds one Pauli code per qubit.
+template <int W, int T>
+__device__ __forceinline__ uint32_t syndrome_bits(const KParams &p, const uint16_t *tab,
+                                                  const uint8_t *cn_sym, const uint8_t *cn_deg,
+                                                  const uint8_t *e, int tid)
+{
+    uint32_t bits = 0;
+    const int nmask = p.n_pad - 1;
+    int t = 0;
+    for (int i = tid; i < p.m; i += T, ++t) {
+        uint32_t x = 0;
+        if constexpr (W > 0) {
+            uint32_t xflag = 0;
+#pragma unroll
+            for (int k = 0; k < 2 * W; ++k) {
+                const uint32_t ent = tab[k * p.m_pad + i];
+                x ^= e[ent & nmask];
+                xflag = ent >> 15;
+            }
+            // X check: anticommutes with the z-bit (code 2 or 3); Z check: x-bit.
+            x = (x >> xflag) & 1u;
+        } else {
+            const int d = cn_deg[i];
+            for (int k = 0; k < d; ++k) {
+                const uint32_t c = e[tab[k * p.m_pad + i] & nmask];
+                const uint32_t s = cn_sym[k * p.m_pad + i];
+                x ^= ((c & 1u) & (s >> 1)) ^ ((c >> 1) & (s & 1u));
+            }
+        }
+        bits |= (x & 1u) << t;
+    }
+    return bits;
+}
+
+// ---- check-node phase (decoder.py:311-338) ---------------------------------
+template <int W, int T, bool BP4>
+__device__ __forceinline__ void cn_phase(const KParams &p, const uint16_t *tab, const uint8_t *cn_deg,
+                                         float *msg, uint32_t syn_bits, uint32_t res_bits, float g0,
+                                         float g1, int tid)
+{
+    const int m = p.m, mp = p.m_pad;
+    int t = 0;
+    for (int i = tid; i < m; i += T, ++t) {
+        const uint32_t sneg = (syn_bits >> t) & 1u;
+        const float gain = ((res_bits >> t) & 1u) ? g1 : g0;
+        if constexpr (W > 0) {
+            constexpr int D = 2 * W;
+            uint32_t slot[D];
+            float v[D];
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                slot[k] = tab[k * mp + i] & 0x7fffu;
+                v[k] = msg[slot[k]];
+            }
+            uint32_t negs = 0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) negs |= (v[k] < 0.0f ? 1u : 0u) << k;
+            const uint32_t par = (__popc(negs) & 1u) ^ sneg;
+            if constexpr (BP4) {
+                float ph[D];
+                OptF o[D];
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    ph[k] = phi(fmaxf(fabsf(v[k]), 1e-12f));
+                    o[k] = OptF{ph[k], true};
+                }
+                const float total = segsum_c<D>(o);
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    float ext = total - ph[k];
+                    ext = ext < 1e-12f ? 1e-12f : (ext > 50.0f ? 50.0f : ext);
+                    const float mag = fminf(phi(ext), kClip);
+                    const uint32_t sb = (par ^ (negs >> k)) & 1u;
+                    msg[slot[k]] = u2f(f2u(mag) | (sb << 31));
+                }
+            } else {
+                float mn1 = __int_as_float(0x7f800000), mn2 = mn1;
+                int idx = 0;
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    const float a = fabsf(v[k]);
+                    mn2 = fminf(mn2, fmaxf(mn1, a));
+                    if (a < mn1) { mn1 = a; idx = k; }
+                }
+                const float m1 = fminf(gain * mn1, kClip), m2 = fminf(gain * mn2, kClip);
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    const float mag = k == idx ? m2 : m1;
+                    const uint32_t sb = (par ^ (negs >> k)) & 1u;
+                    msg[slot[k]] = u2f(f2u(mag) | (sb << 31));
+                }
+            }
+        } else {
+            const int d = cn_deg[i];
+            uint32_t slot[kGenericMaxDeg];
+            float v[kGenericMaxDeg];
+            uint32_t negs = 0;
+            for (int k = 0; k < d; ++k) {
+                slot[k] = tab[k * mp + i];
+                v[k] = msg[slot[k]];
+                negs |= (v[k] < 0.0f ? 1u : 0u) << k;
+            }
+            const uint32_t par = (__popc(negs) & 1u) ^ sneg;
+            if constexpr (BP4) {
+                float ph[kGenericMaxDeg];
+                for (int k = 0; k < d; ++k) ph[k] = phi(fmaxf(fabsf(v[k]), 1e-12f));
+                const float total = segsum_rt(ph, d);
+                for (int k = 0; k < d; ++k) {
+                    float ext = total - ph[k];
+                    ext = ext < 1e-12f ? 1e-12f : (ext > 50.0f ? 50.0f : ext);
+                    const float mag = fminf(phi(ext), kClip);
+                    msg[slot[k]] = u2f(f2u(mag) | (((par ^ (negs >> k)) & 1u) << 31));
+                }
+            } else {
+                float mn1 = __int_as_float(0x7f800000), mn2 = mn1;
+                int idx = 0;
+                for (int k = 0; k < d; ++k) {
+                    const float a = fabsf(v[k]);
+                    mn2 = fminf(mn2, fmaxf(mn1, a));
+                    if (a < mn1) { mn1 = a; idx = k; }
+                }
+                const float m1 = fminf(gain * mn1, kClip), m2 = fminf(gain * mn2, kClip);
+                for (int k = 0; k < d; ++k) {
+                    const float mag = k == idx ? m2 : m1;
+                    msg[slot[k]] = u2f(f2u(mag) | (((par ^ (negs >> k)) & 1u) << 31));
+                }
+            }
+        }
+    }
+}
+
+// ---- qubit-node phase (decoder.py:340-359) + next hard decision ------------
+template <int W, int T, bool ADD>
+__device__ __forceinline__ void vn_phase(const KParams &p, const uint8_t *vn_sym, const uint8_t *vn_deg,
+                                         float *msg, uint8_t *ehat, int tid)
+{
+    const int n = p.n, np_ = p.n_pad;
+    const float l0 = p.l0;
+    for (int j = tid; j < n; j += T) {
+        if constexpr (W > 0) {
+            constexpr int D = 2 * W;
+            float c[D];
+            OptF ox[D], oz[D], oa[D];
+#pragma unroll
+            for (int s = 0; s < D; ++s) {
+                c[s] = msg[s * np_ + j];
+                // anti_Z keeps X-edges (x-bit), anti_X keeps Z-edges (z-bit)
+                ox[s] = OptF{c[s], s >= W};
+                oz[s] = OptF{c[s], s < W};
+                oa[s] = OptF{c[s], true};
+            }
+            const float totX = segsum_c<D>(ox);
+            const float totZ = segsum_c<D>(oz);
+            const float totY = segsum_c<D>(oa);
+            const float bX = l0 + totX, bZ = l0 + totZ;
+            ehat[j] = (uint8_t)hard_decision(bX, bZ, l0 + totY);
+            if constexpr (ADD) {
+#pragma unroll
+                for (int s = 0; s < D; ++s) msg[s * np_ + j] = clip64(l0 + (totY - c[s]));
+            } else {
+                const float selfX = logaddexp(0.0f, -bX);
+                const float selfZ = logaddexp(0.0f, -bZ);
+#pragma unroll
+                for (int s = 0; s < D; ++s) {
+                    // X-edge: b_a1 = b_Z, b_a2 = b_Y; Z-edge: b_a1 = b_X, b_a2 = b_Y
+                    const float ba1 = l0 + ((s < W ? totZ : totX) - c[s]);
+                    const float ba2 = l0 + (totY - c[s]);
+                    const float out = (s < W ? selfX : selfZ) - logaddexp(-ba1, -ba2);
+                    msg[s * np_ + j] = clip64(out);
+                }
+            }
+        } else {
+            const int d = vn_deg[j];
+            float c[kGenericMaxDeg], tmp[kGenericMaxDeg];
+            uint32_t sym[kGenericMaxDeg];
+            for (int s = 0; s < d; ++s) {
+                c[s] = msg[s * np_ + j];
+                sym[s] = vn_sym[s * np_ + j];
+            }
+            float tot[4];
+#pragma unroll
+            for (int e = 1; e <= 3; ++e) {
+                for (int s = 0; s < d; ++s) {
+                    const uint32_t sx = sym[s] & 1u, sz = sym[s] >> 1;
+                    const uint32_t a = e == 1 ? sz : (e == 2 ? sx : (sx ^ sz));
+                    tmp[s] = a ? c[s] : 0.0f;
+                }
+                tot[e] = segsum_rt(tmp, d);
+            }
+            ehat[j] = (uint8_t)hard_decision(l0 + tot[1], l0 + tot[2], l0 + tot[3]);
+            if constexpr (ADD) {
+                for (int s = 0; s < d; ++s) tmp[s] = c[s];
+                const float all = segsum_rt(tmp, d);
+                for (int s = 0; s < d; ++s) msg[s * np_ + j] = clip64(l0 + (all - c[s]));
+            } else {
+                for (int s = 0; s < d; ++s) {
+                    const uint32_t sx = sym[s] & 1u, sz = sym[s] >> 1;
+                    float b[4];
+#pragma unroll
+                    for (int e = 1; e <= 3; ++e) {
+                        const uint32_t a = e == 1 ? sz : (e == 2 ? sx : (sx ^ sz));
+                        b[e] = a ? l0 + (tot[e] - c[s]) : l0 + tot[e];
+                    }
+                    const float bs = sym[s] == 1 ? b[1] : (sym[s] == 3 ? b[3] : b[2]);
+                    const float b1 = sym[s] == 1 ? b[2] : b[1];
+                    const float b2 = sym[s] == 3 ? b[2] : b[3];
+                    msg[s * np_ + j] = clip64(logaddexp(0.0f, -bs) - logaddexp(-b1, -b2));
+                }
+            }
+        }
+    }
+}
+
+template <int T>
+__device__ __forceinline__ void snapshot(const KParams &p, const float *msg, float *dst, int tid)
+{
+    const int total = p.dv_max * p.n_pad;
+    for (int s = tid; s < total; s += T) {
+        const int e = p.slot_edge[s];
+        if (e >= 0) dst[e] = msg[s];
+    }
+}
+
+template <int W, int T, bool BP4, bool ADD>
+__global__ void __launch_bounds__(1024) decode_kernel(const KParams p)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    // ---- per-CTA copy of the graph tables ----
+    {
+        const uint32_t words = p.tab_bytes / 4;
+        const uint32_t *src[5];
+        uint32_t sz[5];
+        const uint32_t tabw = (uint32_t)p.dc_max * p.m_pad / 2;
+        src[0] = (const uint32_t *)p.cn_slot; sz[0] = tabw;
+        int nsrc = 1;
+        if constexpr (W == 0) {
+            src[1] = (const uint32_t *)p.cn_sym; sz[1] = (uint32_t)p.dc_max * p.m_pad / 4;
+            src[2] = (const uint32_t *)p.cn_deg; sz[2] = (uint32_t)p.m_pad / 4;
+            src[3] = (const uint32_t *)p.vn_sym; sz[3] = (uint32_t)p.dv_max * p.n_pad / 4;
+            src[4] = (const uint32_t *)p.vn_deg; sz[4] = (uint32_t)p.n_pad / 4;
+            nsrc = 5;
+        }
+        uint32_t *dst = (uint32_t *)smem;
+        uint32_t off = 0;
+        for (int s = 0; s < nsrc; ++s) {
+            for (uint32_t w = threadIdx.x; w < sz[s]; w += blockDim.x) dst[off + w] = src[s][w];
+            off += sz[s];
+        }
+        (void)words;
+    }
+    __syncthreads();
+    const uint16_t *tab = (const uint16_t *)smem;
+    const uint8_t *cn_sym = nullptr, *cn_deg = nullptr, *vn_sym = nullptr, *vn_deg = nullptr;
+    if constexpr (W == 0) {
+        cn_sym = smem + (size_t)p.dc_max * p.m_pad * 2;
+        cn_deg = cn_sym + (size_t)p.dc_max * p.m_pad;
+        vn_sym = cn_deg + p.m_pad;
+        vn_deg = vn_sym + (size_t)p.dv_max * p.n_pad;
+    }
+
+    const int g = threadIdx.x / T, tid = threadIdx.x % T;
+    unsigned char *gbase = smem + p.tab_bytes + (size_t)g * p.group_bytes;
+    float *msg = (float *)gbase;
+    uint8_t *ehat = gbase + (size_t)p.dv_max * p.n_pad * 4;
+    int *scratch = (int *)(ehat + p.n_pad);  // 2*(T/32) ints + frame slot (2 ints)
+    long long *fslot = (long long *)(scratch + 2 * (T / 32) + ((2 * (T / 32)) & 1));
+
+    const int n = p.n, m = p.m, np_ = p.n_pad;
+    const int msg_words = p.dv_max * np_;
+    long long c_frames = 0, c_fail = 0, c_iters = 0;
+
+    // hard decision with all-zero check messages: argmin(0, L0, L0, L0)
+    const uint8_t hd0 = (uint8_t)hard_decision(p.l0, p.l0, p.l0);
+    const bool capture = p.tr_vn != nullptr || p.tr_cn != nullptr;
+
+    while (true) {
+        long long f;
+        if constexpr (T == 32) {
+            if (tid == 0) f = (long long)atomicAdd(p.queue, 1ull);
+            f = __shfl_sync(0xffffffffu, f, 0);
+        } else {
+            if (tid == 0) *fslot = (long long)atomicAdd(p.queue, 1ull);
+            group_sync<T>(g);
+            f = *fslot;
+            group_sync<T>(g);
+        }
+        if (f >= p.count) break;
+
+        // ---- frame input: observed syndrome bits per owned check ----
+        uint32_t syn_bits;
+        if (p.sample) {
+            const uint64_t key1 = (uint64_t)(p.start + f);
+            const int nblk = (n + 3) >> 2;
+            for (int b = tid; b < nblk; b += T) {
+                const U64x4 w = philox4x64_10((uint64_t)b + 1, p.seed, key1);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (4 * b + q < n) ehat[4 * b + q] = pauli_from_word(w.v[q], p.kx, p.ky, p.kz);
+            }
+            group_sync<T>(g);
+            syn_bits = syndrome_bits<W, T>(p, tab, cn_sym, cn_deg, ehat, tid);
+            group_sync<T>(g);
+        } else {
+            syn_bits = 0;
+            int t = 0;
+            const uint8_t *s_in = p.syn_in + f * (long long)m;
+            for (int i = tid; i < m; i += T, ++t) syn_bits |= (s_in[i] != 0 ? 1u : 0u) << t;
+        }
+        for (int j = tid; j < np_; j += T) ehat[j] = hd0;
+        for (int s = tid; s < msg_words; s += T) msg[s] = p.v0;
+        group_sync<T>(g);
+
+        int recorded = 0, success = 0, iters = p.l_max, n_gamma = 0, n_snap = 0;
+        for (int ell = 1; ell <= p.l_max; ++ell) {
+            const uint32_t res = syn_bits ^ syndrome_bits<W, T>(p, tab, cn_sym, cn_deg, ehat, tid);
+            const int unsat = group_sum<T>(__popc(res), scratch, ell & 1, tid, g);
+            if (p.tr_unsat && tid == 0) p.tr_unsat[f * p.l_max + n_gamma] = unsat;
+            ++n_gamma;
+            if (unsat == 0 && !recorded) {
+                success = 1;
+                iters = ell;
+                recorded = 1;
+                if (p.out_ehat)
+                    for (int j = tid; j < n; j += T) p.out_ehat[f * n + j] = ehat[j];
+            }
+            if (p.early_stop && unsat == 0) break;
+            if (ell == p.l_max) {
+                if (!recorded && p.out_ehat)
+                    for (int j = tid; j < n; j += T) p.out_ehat[f * n + j] = ehat[j];
+                if (!capture) break;
+            }
+            float g0 = 1.0f, g1 = 1.0f;
+            if (p.gain_mode == 1) {
+                g0 = g1 = p.alpha;
+            } else if (p.gain_mode == 2) {
+                const double gamma = (double)unsat / (double)m;
+                const double base = p.amax - (p.amax - p.amin) * gamma;
+                g0 = (float)(base * 1.0);
+                g1 = (float)(base * p.eta);
+            }
+            cn_phase<W, T, BP4>(p, tab, cn_deg, msg, syn_bits, res, g0, g1, tid);
+            group_sync<T>(g);
+            if (capture && p.tr_cn) snapshot<T>(p, msg, p.tr_cn + (f * p.l_max + n_snap) * p.E, tid);
+            vn_phase<W, T, ADD>(p, vn_sym, vn_deg, msg, ehat, tid);
+            group_sync<T>(g);
+            if (capture) {
+                if (p.tr_vn) snapshot<T>(p, msg, p.tr_vn + (f * p.l_max + n_snap) * p.E, tid);
+                ++n_snap;
+            }
+        }
+        if (tid == 0) {
+            if (p.out_flag) p.out_flag[f] = (uint8_t)(p.sample ? !success : success);
+            if (p.out_iters) p.out_iters[f] = iters;
+            if (p.tr_counts) { p.tr_counts[2 * f] = n_gamma; p.tr_counts[2 * f + 1] = n_snap; }
+        }
+        ++c_frames;
+        c_fail += !success;
+        c_iters += iters;
+        group_sync<T>(g);  // ehat/msg reuse by the next frame
+    }
+    if (p.counters && tid == 0 && c_frames) {
+        atomicAdd((unsigned long long *)&p.counters[0], (unsigned long long)c_frames);
+        atomicAdd((unsigned long long *)&p.counters[1], (unsigned long long)c_fail);
+        atomicAdd((unsigned long long *)&p.counters[2], (unsigned long long)c_iters);
+        atomicAdd((unsigned long long *)&p.counters[3],
+                  (unsigned long long)(p.E * (c_iters - c_frames)));
+    }
+}
+
+}  // namespace qsg

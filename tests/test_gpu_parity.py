@@ -1,0 +1,163 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle.
+
+The bar ("Numerics contract"):
+  * sampling, syndromes, success flags, iteration counts and e_hat are
+    bit-exact against the oracle's fp32 restatement (and against the
+    reference's own golden outcomes where the fp32 restatement matches fp64);
+  * fp32 message snapshots are identical to the oracle's fp32 restatement
+    (float equality, i.e. +0 == -0) on every iteration.
+"""
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GB126, GB254, GB1022, SMALL, TOY, make_tree_rows
+
+pytestmark = pytest.mark.gpu
+
+GAIN = (0.30, 0.50, 1.10)
+CFGS = [("bp4", {}), ("ms", {}), ("sms", {"alpha": 0.75}), ("sagms", {"gain": GAIN})]
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2605_10433_b200 as P
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    return P
+
+
+def _cfg(P, variant, kw, **extra):
+    kw = dict(kw)
+    if "gain" in kw:
+        kw["gain"] = P.GainParams(*kw["gain"])
+    return P.DecoderConfig(variant, **kw, **extra)
+
+
+def digest(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:16]
+
+
+def test_sampler_pin_and_oracle(P, oracle):
+    # reference test_channel.py:82-86 regression pin
+    head = P.sample_error(P.DepolarizingChannel(0.2, 1234), 16, 0).tolist()
+    assert head == [0, 0, 0, 0, 0, 1, 3, 0, 0, 0, 0, 0, 0, 0, 0, 0]
+    for n, eps, seed, start, count in [(254, 0.05, 0, 0, 10_000), (1022, 0.08, 7, 12345, 333),
+                                       (6, 0.5, 2718, 0, 100), (13, 0.0, 5, 0, 10),
+                                       (254, 0.7, 2**64 - 1, 2**40, 50)]:
+        got = P.sample_errors(P.DepolarizingChannel(eps, seed % 2**64), n, start, count)
+        want = oracle.sample_errors(n, eps, seed, start, count)
+        assert np.array_equal(got, want), (n, eps, seed)
+    e = P.sample_errors(P.DepolarizingChannel(0.05, 0), 254, 0, 10_000)
+    assert digest(e) == "538be80789ccb78c"  # SURVEY.md Appendix B error-batch digest
+
+
+def test_syndromes_of(P, oracle):
+    g = P.gb_graph(P.GbSpec(*GB254))
+    dg = P.device_graph(g)
+    e = P.sample_errors_device(254, 0.05, 0, 0, 10_000)
+    syn = torch.empty((10_000, 254), dtype=torch.uint8, device=e.device)
+    from paper_2605_10433_b200 import _native
+    _native.check(_native.lib().qsg_syndromes_of(dg.handle, e.data_ptr(), 10_000, syn.data_ptr(),
+                                                 torch.cuda.current_stream().cuda_stream))
+    s = syn.cpu().numpy()
+    assert digest(s) == "c17effa585aba6c2"
+    assert np.array_equal(s, oracle.syndromes_of(g, e.cpu().numpy()))
+
+
+def test_config1_golden(P, oracle):
+    """BASELINE config 1: [[254,28]] SAGMS p=0.05 seed 0, 1e4 frames, l_max 100."""
+    g = P.gb_graph(P.GbSpec(*GB254))
+    assert g.kind == 5
+    cfg = _cfg(P, "sagms", {"gain": GAIN}, l_max=100)
+    fails, iters, ehat = P.decode_frames_device(g, cfg, 0.05, 0.05, 0, 0, 10_000, want_ehat=True)
+    fails, iters, ehat = fails.cpu().numpy(), iters.cpu().numpy(), ehat.cpu().numpy()
+    assert np.nonzero(fails)[0].tolist() == [356, 813, 951, 3063, 3175, 4838, 5302, 5579, 6030,
+                                             6972, 7982, 8244]
+    assert int(iters.sum()) == 45_097
+    assert digest(ehat) == "851c8b33a191d199"
+    of, oi, oe, _ = oracle.frames(g, cfg, 0.05, 0.05, 0, 0, 10_000, want_ehat=True)
+    assert np.array_equal(fails.astype(bool), of) and np.array_equal(iters, oi) and np.array_equal(ehat, oe)
+    # counters path
+    cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+    P.decode_frames_device(g, cfg, 0.05, 0.05, 0, 0, 10_000, counters=cnt, want_frames=False)
+    assert cnt.cpu().tolist() == [10_000, 12, 45_097, 2540 * (45_097 - 10_000)]
+
+
+@pytest.mark.parametrize("spec,eps,B", [(TOY, 0.1, 300), (SMALL, 0.12, 300), (GB126, 0.06, 400),
+                                        (GB254, 0.08, 300), (GB1022, 0.06, 48)])
+@pytest.mark.parametrize("vn_mode", ["marginal", "additive"])
+@pytest.mark.parametrize("variant,kw", CFGS)
+def test_decode_batch_bit_exact(P, oracle, spec, eps, B, vn_mode, variant, kw):
+    g = P.gb_graph(P.GbSpec(*spec))
+    e = oracle.sample_errors(g.n, eps, 11, 0, B)
+    syn = oracle.syndromes_of(g, e)
+    cfg = _cfg(P, variant, kw, l_max=25, vn_mode=vn_mode)
+    prior = P.prior_llr(eps)
+    got = P.decode_batch(g, syn, prior, cfg, collect_gamma=True)
+    want = oracle.decode(g, syn, prior.llr, cfg, precision=32, trace=True)
+    assert np.array_equal(got.success, want.success)
+    assert np.array_equal(got.iterations, want.iterations)
+    assert np.array_equal(got.e_hat, want.e_hat)
+    for a, b in zip(got.gamma_traces, want.gamma_traces(g.m)):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_generic_graphs_bit_exact(P, oracle, seed):
+    """Non-bicycle graphs (trees, random GB with |a| != |b|) use the generic
+    table-driven kernels."""
+    rng = np.random.default_rng(seed)
+    if seed % 2:
+        n, rows = make_tree_rows(rng, int(rng.integers(5, 14)))
+        g = P.csr_graph(n, rows)
+    else:
+        ell = int(rng.integers(4, 12))
+        a = tuple(sorted(rng.choice(ell, size=int(rng.integers(1, 4)), replace=False).tolist()))
+        b = tuple(sorted(rng.choice(ell, size=int(rng.integers(2, 5)), replace=False).tolist()))
+        g = P.gb_graph(P.GbSpec(ell, a, b))
+    syn = rng.integers(0, 2, size=(170, g.m)).astype(np.uint8)
+    for variant, kw in CFGS:
+        for vn_mode in ("marginal", "additive"):
+            cfg = _cfg(P, variant, kw, l_max=9, vn_mode=vn_mode)
+            l0 = float(rng.uniform(0.5, 5.0))
+            prior = P.ChannelPrior(0.1, l0)
+            got = P.decode_batch(g, syn, prior, cfg)
+            want = oracle.decode(g, syn, l0, cfg, precision=32)
+            assert np.array_equal(got.success, want.success), (variant, vn_mode)
+            assert np.array_equal(got.iterations, want.iterations), (variant, vn_mode)
+            assert np.array_equal(got.e_hat, want.e_hat), (variant, vn_mode)
+
+
+@pytest.mark.parametrize("spec", [SMALL, GB126, GB254])
+@pytest.mark.parametrize("variant,kw", CFGS)
+@pytest.mark.parametrize("vn_mode", ["marginal", "additive"])
+def test_message_snapshots_bit_exact(P, oracle, spec, variant, kw, vn_mode):
+    g = P.gb_graph(P.GbSpec(*spec))
+    e = oracle.sample_errors(g.n, 0.08, 3, 0, 4)
+    syn = oracle.syndromes_of(g, e)
+    cfg = _cfg(P, variant, kw, l_max=6, vn_mode=vn_mode)
+    prior = P.prior_llr(0.08)
+    for f in range(4):
+        got = P.decode(None, g, syn[f], prior, cfg, capture_messages=True, early_stop=False)
+        want = oracle.decode(g, syn[f:f + 1], prior.llr, cfg, precision=32, capture=True,
+                             early_stop=False)
+        assert len(got.message_trace) == want.counts[0, 1]
+        for k, st in enumerate(got.message_trace):
+            assert st.iteration == k + 1
+            assert np.array_equal(st.vn_to_cn.astype(np.float32), want.vn_msgs[0, k])
+            assert np.array_equal(st.cn_to_vn.astype(np.float32), want.cn_msgs[0, k])
+
+
+def test_persistent_queue_partition_invariance(P):
+    """Frames are independent of launch size / start offset (batch-partition
+    invariance, reference test_decoder.py:384-396)."""
+    g = P.gb_graph(P.GbSpec(*GB254))
+    cfg = _cfg(P, "sagms", {"gain": GAIN}, l_max=100)
+    whole = P.decode_frames(g, cfg, 0.08, 0.08, 9, 0, 3000)
+    parts = [P.decode_frames(g, cfg, 0.08, 0.08, 9, s, c) for s, c in [(0, 1), (1, 999), (1000, 2000)]]
+    assert np.array_equal(whole[0], np.concatenate([p[0] for p in parts]))
+    assert np.array_equal(whole[1], np.concatenate([p[1] for p in parts]))
