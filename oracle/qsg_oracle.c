@@ -105,6 +105,7 @@ void qsgo_syndromes_of(const qsgo_graph *g, const uint8_t *e, int64_t B, uint8_t
 #define PHI(x) qo_phi(x)
 #define MAXR(a, b) fmaxf((a), (b))
 #define ABSR(x) fabsf(x)
+#define VN_FACTORED 1
 #include "qsg_oracle_body.h"
 #undef REAL
 #undef SFX
@@ -113,6 +114,7 @@ void qsgo_syndromes_of(const qsgo_graph *g, const uint8_t *e, int64_t B, uint8_t
 #undef PHI
 #undef MAXR
 #undef ABSR
+#undef VN_FACTORED
 
 /* ---- fp64 with glibc: the reference's own arithmetic ---- */
 static inline double lae64(double x, double y) /* npy_logaddexp */
@@ -129,6 +131,7 @@ static inline double lae64(double x, double y) /* npy_logaddexp */
 #define PHI(x) log1p(2.0 / expm1(x))
 #define MAXR(a, b) fmax((a), (b))
 #define ABSR(x) fabs(x)
+#define VN_FACTORED 0
 #include "qsg_oracle_body.h"
 
 void qsgo_math32_batch(int32_t which, const float *x, const float *y, float *out, int64_t n)

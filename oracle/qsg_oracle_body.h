@@ -6,7 +6,7 @@
  * reductions (cv * anti mask, then numpy's pairwise reduceat tree).
  *
  * Required macros: REAL, SFX (32 or 64), TRACE_T, LAE(x, y), PHI(x),
- *                  MAXR(a, b), ABSR(x)
+ *                  MAXR(a, b), ABSR(x), VN_FACTORED (0 = literal decoder.py:348-357)
  */
 
 #define QO_CAT2(a, b) a##b
@@ -182,6 +182,22 @@ static void QF(_decode_one)(const qsgo_graph *g, const qsgo_cfg *cfg, REAL l0, R
                         s->tmp[q] = s->cv[q] * QF(_anti)(e, g->edge_sym[g->vn_order[p0 + q]]);
                     tot[e] = QF(_segsum)(s->tmp, d);
                 }
+#if VN_FACTORED
+                /* fp32 restatement: both anticommuting beliefs of an edge
+                 * contain its own message c, and logaddexp(u - c, v - c) =
+                 * logaddexp(u, v) - c, so out = V[sym] - c with V[S] =
+                 * LAE(0, -(l0 + tot_S)) - LAE(-(l0 + tot_a1), -(l0 + tot_a2))
+                 * once per qubit and symbol (a1/a2 as selected at :355-356). */
+                REAL V[4];
+                for (int S = 1; S <= 3; ++S) {
+                    int a1 = S == 1 ? 2 : 1, a2 = S == 3 ? 2 : 3;
+                    V[S] = LAE((REAL)0.0, -(l0 + tot[S])) - LAE(-(l0 + tot[a1]), -(l0 + tot[a2]));
+                }
+                for (int64_t q = 0; q < d; ++q) {
+                    uint8_t sym = g->edge_sym[g->vn_order[p0 + q]];
+                    s->vmsg[g->vn_order[p0 + q]] = QF(_clip)(V[sym] - s->cv[q], -CLIP, CLIP);
+                }
+#else
                 for (int64_t q = 0; q < d; ++q) {
                     uint8_t sym = g->edge_sym[g->vn_order[p0 + q]];
                     REAL c = s->cv[q], b[4];
@@ -192,6 +208,7 @@ static void QF(_decode_one)(const qsgo_graph *g, const qsgo_cfg *cfg, REAL l0, R
                     REAL out = LAE((REAL)0.0, -b_self) - LAE(-b_a1, -b_a2);
                     s->vmsg[g->vn_order[p0 + q]] = QF(_clip)(out, -CLIP, CLIP);
                 }
+#endif
             }
         }
         if (capture) {

@@ -61,7 +61,7 @@ int upload(T **dst, const std::vector<T> &src)
 
 void free_device(qsg_graph *g)
 {
-    cudaFree(g->d_cn_slot); cudaFree(g->d_cn_sym); cudaFree(g->d_cn_deg);
+    cudaFree(g->d_cn_tab);
     cudaFree(g->d_vn_sym); cudaFree(g->d_vn_deg); cudaFree(g->d_slot_edge);
     cudaFree(g->d_cn_ptr); cudaFree(g->d_edge_vn); cudaFree(g->d_edge_sym);
 }
@@ -132,7 +132,7 @@ int compile_layout(qsg_graph *g, int32_t n, int32_t m, const int64_t *cn_ptr, co
 
     // kernel kind
     int kind = 0;
-    if (dv_max % 2 == 0 && bicycle_w_supported(dv_max / 2) && (int64_t)dv_max * g->n_pad <= 32768) {
+    if (dv_max % 2 == 0 && bicycle_w_supported(dv_max / 2) && (int64_t)dv_max * g->n_pad * 4 < (1 << 24)) {
         const int W = dv_max / 2;
         bool ok = true;
         for (int i = 0; i < m && ok; ++i) {
@@ -151,8 +151,8 @@ int compile_layout(qsg_graph *g, int32_t n, int32_t m, const int64_t *cn_ptr, co
     if (kind == 0) {
         if (dc_max > qsg::kGenericMaxDeg || dv_max > qsg::kGenericMaxDeg)
             return fail(QSG_EUNSUPPORTED, "node degree exceeds the generic kernel limit (32)");
-        if ((int64_t)dv_max * g->n_pad > 65535)
-            return fail(QSG_EUNSUPPORTED, "graph too large for 16-bit slot tables");
+        if ((int64_t)dv_max * g->n_pad * 4 >= (1 << 24))
+            return fail(QSG_EUNSUPPORTED, "graph too large for 24-bit slot offsets");
     }
     // threads per frame: every thread owns <= 32 checks (register bit masks)
     const int nodes = std::max(n, m);
@@ -160,21 +160,24 @@ int compile_layout(qsg_graph *g, int32_t n, int32_t m, const int64_t *cn_ptr, co
     else if (m <= 128 * 32) g->threads = 128;
     else return fail(QSG_EUNSUPPORTED, "more than 4096 checks");
 
-    // check slot table, k-major [dc_max][m_pad]
+    // check table: one row of row_words (odd) u32 per check: byte offsets of
+    // the check's edges in canonical order (generic rows also carry the edge
+    // symbol in bits 30-31) and an info word at index dc_max (bicycle: 1 for
+    // X checks, 0 for Z checks; generic: the degree).
     const int mp = g->m_pad, np_ = g->n_pad;
-    std::vector<uint16_t> cn_slot((size_t)dc_max * mp, 0);
-    std::vector<uint8_t> cn_sym((size_t)dc_max * mp, 0), cn_deg(mp, 0);
+    int rw = dc_max + 1;
+    if (rw % 2 == 0) ++rw;
+    g->row_words = rw;
+    std::vector<uint32_t> cn_tab((size_t)mp * rw, 0);
     std::vector<uint8_t> vn_sym((size_t)dv_max * np_, 0), vn_deg(np_, 0);
     std::vector<int32_t> slot_edge((size_t)dv_max * np_, -1);
     for (int i = 0; i < m; ++i) {
-        cn_deg[i] = (uint8_t)(cn_ptr[i + 1] - cn_ptr[i]);
+        uint32_t *row = &cn_tab[(size_t)i * rw];
+        row[dc_max] = kind > 0 ? (edge_sym[cn_ptr[i]] == 1 ? 1u : 0u) : (uint32_t)(cn_ptr[i + 1] - cn_ptr[i]);
         for (int64_t e = cn_ptr[i]; e < cn_ptr[i + 1]; ++e) {
             const int k = (int)(e - cn_ptr[i]);
             const uint32_t slot = (uint32_t)pos_in_vn[e] * np_ + (uint32_t)edge_vn[e];
-            uint32_t ent = slot;
-            if (kind > 0 && edge_sym[e] == 1) ent |= 0x8000u;
-            cn_slot[(size_t)k * mp + i] = (uint16_t)ent;
-            cn_sym[(size_t)k * mp + i] = edge_sym[e];
+            row[k] = slot * 4u | (kind > 0 ? 0u : (uint32_t)edge_sym[e] << 30);
             slot_edge[slot] = (int32_t)e;
         }
     }
@@ -188,11 +191,9 @@ int compile_layout(qsg_graph *g, int32_t n, int32_t m, const int64_t *cn_ptr, co
         return QSG_OK;
     }
     int rc;
-    if ((rc = upload(&g->d_cn_slot, cn_slot)) || (rc = upload(&g->d_slot_edge, slot_edge))) return rc;
+    if ((rc = upload(&g->d_cn_tab, cn_tab)) || (rc = upload(&g->d_slot_edge, slot_edge))) return rc;
     if (kind == 0) {
-        if ((rc = upload(&g->d_cn_sym, cn_sym)) || (rc = upload(&g->d_cn_deg, cn_deg)) ||
-            (rc = upload(&g->d_vn_sym, vn_sym)) || (rc = upload(&g->d_vn_deg, vn_deg)))
-            return rc;
+        if ((rc = upload(&g->d_vn_sym, vn_sym)) || (rc = upload(&g->d_vn_deg, vn_deg))) return rc;
     }
     std::vector<int32_t> cp32(g->cn_ptr.begin(), g->cn_ptr.end()), ev32(g->edge_vn.begin(), g->edge_vn.end());
     if ((rc = upload(&g->d_cn_ptr, cp32)) || (rc = upload(&g->d_edge_vn, ev32)) ||
@@ -200,11 +201,11 @@ int compile_layout(qsg_graph *g, int32_t n, int32_t m, const int64_t *cn_ptr, co
         return rc;
 
     // shared-memory footprint
-    size_t tab = (size_t)dc_max * mp * 2;
-    if (kind == 0) tab += (size_t)dc_max * mp + mp + (size_t)dv_max * np_ + np_;
+    size_t tab = (size_t)mp * rw * 4;
+    if (kind == 0) tab += (size_t)dv_max * np_ + np_;
     g->tab_bytes = (uint32_t)((tab + 15) / 16 * 16);
     const int T = g->threads;
-    size_t grp = (size_t)dv_max * np_ * 4 + np_ + 2 * (T / 32) * 4 + 8;
+    size_t grp = (size_t)dv_max * np_ * 4 + (size_t)np_ * 4 + 2 * (T / 32) * 4 + 8;
     g->group_bytes = (uint32_t)((grp + 15) / 16 * 16);
     return QSG_OK;
 }
@@ -244,7 +245,7 @@ int launch_cfg(qsg_graph *g, bool bp4, bool add, void *fn, qsg::LaunchCfg *out)
     int max_smem = 0;
     QSG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
     const int T = g->threads;
-    const int gmax = T == 32 ? 16 : 8;
+    const int gmax = T == 32 ? 16 : 4;  // __launch_bounds__(512)
     qsg::LaunchCfg best;
     for (int G = 1; G <= gmax; ++G) {
         const size_t smem = g->tab_bytes + (size_t)G * g->group_bytes;
@@ -288,10 +289,10 @@ int launch_decode(qsg_graph *g, const qsg_decoder_cfg *cfg, qsg::KParams &p, cud
 
 void fill_graph_params(const qsg_graph *g, qsg::KParams &p)
 {
-    p.cn_slot = g->d_cn_slot; p.cn_sym = g->d_cn_sym; p.cn_deg = g->d_cn_deg;
+    p.cn_tab = g->d_cn_tab;
     p.vn_sym = g->d_vn_sym; p.vn_deg = g->d_vn_deg; p.slot_edge = g->d_slot_edge;
     p.n = g->n; p.m = g->m; p.n_pad = g->n_pad; p.log2_npad = g->log2_npad; p.m_pad = g->m_pad;
-    p.dc_max = g->dc_max; p.dv_max = g->dv_max; p.E = g->E;
+    p.dc_max = g->dc_max; p.dv_max = g->dv_max; p.row_words = g->row_words; p.E = g->E;
     p.tab_bytes = g->tab_bytes; p.group_bytes = g->group_bytes;
 }
 

@@ -42,14 +42,14 @@ struct qsg_graph {
     int32_t n = 0, m = 0;
     int64_t E = 0;
     int32_t dc_max = 0, dv_max = 0, kind = 0, threads = 32;
-    int32_t n_pad = 0, log2_npad = 0, m_pad = 0;
+    int32_t n_pad = 0, log2_npad = 0, m_pad = 0, row_words = 0;
     int32_t num_sms = 0;
     // canonical TannerGraph arrays (host)
     std::vector<int64_t> edge_cn, edge_vn, cn_ptr, vn_order, vn_ptr;
     std::vector<uint8_t> edge_sym;
     // device tables
-    uint16_t *d_cn_slot = nullptr;
-    uint8_t *d_cn_sym = nullptr, *d_cn_deg = nullptr, *d_vn_sym = nullptr, *d_vn_deg = nullptr;
+    uint32_t *d_cn_tab = nullptr;
+    uint8_t *d_vn_sym = nullptr, *d_vn_deg = nullptr;
     int32_t *d_slot_edge = nullptr;
     int32_t *d_cn_ptr = nullptr, *d_edge_vn = nullptr;
     uint8_t *d_edge_sym = nullptr;

@@ -18,10 +18,11 @@
 // owned by exactly one check and one qubit, and the C and V phases are
 // separated by group barriers).  Slot of the s-th edge of qubit j (qubit
 // order = ascending check index, code.py:171) is s * n_pad + j, so qubit
-// reads/writes are unit-stride across the group (conflict-free) and check
-// reads go through a per-graph u16 slot table (k-major, also conflict-free
-// for circulant codes).  Canonical edge order only matters for the BP4 phi
-// sum; the table lists each check's edges in canonical order.
+// reads/writes are unit-stride across the group (conflict-free).  Checks
+// reach their edges through a per-graph table of byte offsets, one row of
+// `row_words` (odd, so rows start in distinct banks) u32 words per check:
+// entries 0..d-1 in canonical order (the order of the BP4 phi sum) and an
+// info word at index dc_max.  Hard decisions are kept as one u32 per qubit.
 //
 // W > 0 selects the "bicycle" specialisation (all degrees 2W, each qubit's
 // edges X-then-Z, single-symbol checks: every GB code with |a| = |b| = W),
@@ -40,13 +41,11 @@ constexpr int kGenericMaxDeg = 32;
 
 struct KParams {
     // graph tables (global; copied to shared memory per CTA)
-    const uint16_t *cn_slot;   // [dc_max][m_pad]
-    const uint8_t *cn_sym;     // [dc_max][m_pad] generic only
-    const uint8_t *cn_deg;     // [m_pad]         generic only
+    const uint32_t *cn_tab;    // [m_pad][row_words] byte offsets (+ sym << 30 generic) + info
     const uint8_t *vn_sym;     // [dv_max][n_pad] generic only
     const uint8_t *vn_deg;     // [n_pad]         generic only
     const int32_t *slot_edge;  // [dv_max*n_pad]  canonical edge per slot (traces)
-    int32_t n, m, n_pad, log2_npad, m_pad, dc_max, dv_max;
+    int32_t n, m, n_pad, log2_npad, m_pad, dc_max, dv_max, row_words;
     int64_t E;
     // decoder
     int32_t gain_mode;  // 0: none (bp4/ms), 1: constant alpha (sms), 2: sagms
@@ -186,34 +185,51 @@ __device__ __forceinline__ int group_sum(int v, int *scratch, int parity, int ti
     }
 }
 
+// Shared-memory view of one group (frame) plus the per-CTA tables.
+struct GroupMem {
+    const uint32_t *tab;     // check rows (byte offsets into msg)
+    const uint8_t *vn_sym;   // generic only
+    const uint8_t *vn_deg;   // generic only
+    unsigned char *msg;      // fp32 messages, slot-major
+    uint32_t *ehat;          // one Pauli code per qubit
+};
+
+__device__ __forceinline__ float lds_f(const unsigned char *base, uint32_t off)
+{
+    return *reinterpret_cast<const float *>(base + off);
+}
+__device__ __forceinline__ void sts_u(unsigned char *base, uint32_t off, uint32_t v)
+{
+    *reinterpret_cast<uint32_t *>(base + off) = v;
+}
+
 // Residual (or syndrome) bits of this thread's checks; bit t <-> check
-// tid + t*T.  e[] holds one Pauli code per qubit.
+// tid + t*T.  gm.ehat holds one Pauli code per qubit.  For a check with
+// single symbol S the parity of trace(e_j, S) is one bit of the XOR of the
+// codes (z-bit for X checks, x-bit for Z checks), decoder.py:303-309.
 template <int W, int T>
-__device__ __forceinline__ uint32_t syndrome_bits(const KParams &p, const uint16_t *tab,
-                                                  const uint8_t *cn_sym, const uint8_t *cn_deg,
-                                                  const uint8_t *e, int tid)
+__device__ __forceinline__ uint32_t syndrome_bits(const KParams &p, const GroupMem &gm, int tid)
 {
     uint32_t bits = 0;
-    const int nmask = p.n_pad - 1;
+    const uint32_t jmask = (uint32_t)(p.n_pad - 1) << 2;
+    const unsigned char *eb = reinterpret_cast<const unsigned char *>(gm.ehat);
     int t = 0;
+#pragma unroll 1
     for (int i = tid; i < p.m; i += T, ++t) {
+        const uint32_t *row = gm.tab + i * p.row_words;
         uint32_t x = 0;
         if constexpr (W > 0) {
-            uint32_t xflag = 0;
 #pragma unroll
-            for (int k = 0; k < 2 * W; ++k) {
-                const uint32_t ent = tab[k * p.m_pad + i];
-                x ^= e[ent & nmask];
-                xflag = ent >> 15;
-            }
-            // X check: anticommutes with the z-bit (code 2 or 3); Z check: x-bit.
-            x = (x >> xflag) & 1u;
+            for (int k = 0; k < 2 * W; ++k)
+                x ^= *reinterpret_cast<const uint32_t *>(eb + (row[k] & jmask));
+            x >>= row[p.dc_max];  // info word: 1 for X checks, 0 for Z checks
         } else {
-            const int d = cn_deg[i];
+            const int d = (int)row[p.dc_max];
             for (int k = 0; k < d; ++k) {
-                const uint32_t c = e[tab[k * p.m_pad + i] & nmask];
-                const uint32_t s = cn_sym[k * p.m_pad + i];
-                x ^= ((c & 1u) & (s >> 1)) ^ ((c >> 1) & (s & 1u));
+                const uint32_t ent = row[k];
+                const uint32_t c = *reinterpret_cast<const uint32_t *>(eb + (ent & jmask));
+                const uint32_t sym = ent >> 30;
+                x ^= ((c & 1u) & (sym >> 1)) ^ ((c >> 1) & (sym & 1u));
             }
         }
         bits |= (x & 1u) << t;
@@ -222,29 +238,35 @@ __device__ __forceinline__ uint32_t syndrome_bits(const KParams &p, const uint16
 }
 
 // ---- check-node phase (decoder.py:311-338) ---------------------------------
+// Min-sum: the argmin edge gets min2 and all others min1, with ties at min1
+// giving min2 == min1; so mag_e = (|v_e| == min1 ? min2 : min1) reproduces
+// the first-argmin rule (:325-333) without tracking the index.  Signs: the
+// extrinsic sign is (-1)^s_i * prod(sgn) * sgn_e (:314-316); messages are
+// never -0.0, so sgn_e is the IEEE sign bit and the product is an XOR.
 template <int W, int T, bool BP4>
-__device__ __forceinline__ void cn_phase(const KParams &p, const uint16_t *tab, const uint8_t *cn_deg,
-                                         float *msg, uint32_t syn_bits, uint32_t res_bits, float g0,
-                                         float g1, int tid)
+__device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, uint32_t syn_bits,
+                                         uint32_t res_bits, float g0, float g1, int tid)
 {
-    const int m = p.m, mp = p.m_pad;
+    constexpr uint32_t kAddr = 0x00ffffffu;  // generic entries carry sym << 30
+    unsigned char *msg = gm.msg;
     int t = 0;
-    for (int i = tid; i < m; i += T, ++t) {
-        const uint32_t sneg = (syn_bits >> t) & 1u;
+#pragma unroll 1
+    for (int i = tid; i < p.m; i += T, ++t) {
+        const uint32_t *row = gm.tab + i * p.row_words;
+        const uint32_t sneg = ((syn_bits >> t) & 1u) << 31;
         const float gain = ((res_bits >> t) & 1u) ? g1 : g0;
         if constexpr (W > 0) {
             constexpr int D = 2 * W;
-            uint32_t slot[D];
+            uint32_t off[D];
             float v[D];
+            uint32_t sx = sneg;
 #pragma unroll
             for (int k = 0; k < D; ++k) {
-                slot[k] = tab[k * mp + i] & 0x7fffu;
-                v[k] = msg[slot[k]];
+                off[k] = row[k];
+                v[k] = lds_f(msg, off[k]);
+                sx ^= f2u(v[k]);
             }
-            uint32_t negs = 0;
-#pragma unroll
-            for (int k = 0; k < D; ++k) negs |= (v[k] < 0.0f ? 1u : 0u) << k;
-            const uint32_t par = (__popc(negs) & 1u) ^ sneg;
+            const uint32_t sgn = sx & 0x80000000u;  // (-1)^s_i * prod sgn, as a sign bit
             if constexpr (BP4) {
                 float ph[D];
                 OptF o[D];
@@ -256,62 +278,58 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const uint16_t *tab, 
                 const float total = segsum_c<D>(o);
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
-                    float ext = total - ph[k];
-                    ext = ext < 1e-12f ? 1e-12f : (ext > 50.0f ? 50.0f : ext);
-                    const float mag = fminf(phi(ext), kClip);
-                    const uint32_t sb = (par ^ (negs >> k)) & 1u;
-                    msg[slot[k]] = u2f(f2u(mag) | (sb << 31));
+                    const float ext = fminf(fmaxf(total - ph[k], 1e-12f), 50.0f);
+                    const uint32_t mag = f2u(fminf(phi(ext), kClip)) ^ sgn;
+                    sts_u(msg, off[k], (f2u(v[k]) & 0x80000000u) ^ mag);
                 }
             } else {
-                float mn1 = __int_as_float(0x7f800000), mn2 = mn1;
-                int idx = 0;
+                float mn1 = fabsf(v[0]), mn2 = __int_as_float(0x7f800000);
 #pragma unroll
-                for (int k = 0; k < D; ++k) {
+                for (int k = 1; k < D; ++k) {
                     const float a = fabsf(v[k]);
                     mn2 = fminf(mn2, fmaxf(mn1, a));
-                    if (a < mn1) { mn1 = a; idx = k; }
+                    mn1 = fminf(mn1, a);
                 }
-                const float m1 = fminf(gain * mn1, kClip), m2 = fminf(gain * mn2, kClip);
+                const uint32_t m1 = f2u(fminf(gain * mn1, kClip)) ^ sgn;
+                const uint32_t m2 = f2u(fminf(gain * mn2, kClip)) ^ sgn;
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
-                    const float mag = k == idx ? m2 : m1;
-                    const uint32_t sb = (par ^ (negs >> k)) & 1u;
-                    msg[slot[k]] = u2f(f2u(mag) | (sb << 31));
+                    const uint32_t mag = fabsf(v[k]) == mn1 ? m2 : m1;
+                    sts_u(msg, off[k], (f2u(v[k]) & 0x80000000u) ^ mag);
                 }
             }
         } else {
-            const int d = cn_deg[i];
-            uint32_t slot[kGenericMaxDeg];
+            const int d = (int)row[p.dc_max];
+            uint32_t off[kGenericMaxDeg];
             float v[kGenericMaxDeg];
-            uint32_t negs = 0;
+            uint32_t sx = sneg;
             for (int k = 0; k < d; ++k) {
-                slot[k] = tab[k * mp + i];
-                v[k] = msg[slot[k]];
-                negs |= (v[k] < 0.0f ? 1u : 0u) << k;
+                off[k] = row[k] & kAddr;
+                v[k] = lds_f(msg, off[k]);
+                sx ^= f2u(v[k]);
             }
-            const uint32_t par = (__popc(negs) & 1u) ^ sneg;
+            const uint32_t sgn = sx & 0x80000000u;
             if constexpr (BP4) {
                 float ph[kGenericMaxDeg];
                 for (int k = 0; k < d; ++k) ph[k] = phi(fmaxf(fabsf(v[k]), 1e-12f));
                 const float total = segsum_rt(ph, d);
                 for (int k = 0; k < d; ++k) {
-                    float ext = total - ph[k];
-                    ext = ext < 1e-12f ? 1e-12f : (ext > 50.0f ? 50.0f : ext);
-                    const float mag = fminf(phi(ext), kClip);
-                    msg[slot[k]] = u2f(f2u(mag) | (((par ^ (negs >> k)) & 1u) << 31));
+                    const float ext = fminf(fmaxf(total - ph[k], 1e-12f), 50.0f);
+                    const uint32_t mag = f2u(fminf(phi(ext), kClip)) ^ sgn;
+                    sts_u(msg, off[k], (f2u(v[k]) & 0x80000000u) ^ mag);
                 }
             } else {
                 float mn1 = __int_as_float(0x7f800000), mn2 = mn1;
-                int idx = 0;
                 for (int k = 0; k < d; ++k) {
                     const float a = fabsf(v[k]);
                     mn2 = fminf(mn2, fmaxf(mn1, a));
-                    if (a < mn1) { mn1 = a; idx = k; }
+                    mn1 = fminf(mn1, a);
                 }
-                const float m1 = fminf(gain * mn1, kClip), m2 = fminf(gain * mn2, kClip);
+                const uint32_t m1 = f2u(fminf(gain * mn1, kClip)) ^ sgn;
+                const uint32_t m2 = f2u(fminf(gain * mn2, kClip)) ^ sgn;
                 for (int k = 0; k < d; ++k) {
-                    const float mag = k == idx ? m2 : m1;
-                    msg[slot[k]] = u2f(f2u(mag) | (((par ^ (negs >> k)) & 1u) << 31));
+                    const uint32_t mag = fabsf(v[k]) == mn1 ? m2 : m1;
+                    sts_u(msg, off[k], (f2u(v[k]) & 0x80000000u) ^ mag);
                 }
             }
         }
@@ -319,54 +337,60 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const uint16_t *tab, 
 }
 
 // ---- qubit-node phase (decoder.py:340-359) + next hard decision ------------
+// Marginal mode: both anticommuting beliefs of an edge contain that edge's
+// own message c (b_a = l0 + tot_a - c), and logaddexp(u - c, v - c) =
+// logaddexp(u, v) - c, so out = V[sym] - c with
+//   V[S] = LAE(0, -(l0 + tot_S)) - LAE(-(l0 + tot_a1), -(l0 + tot_a2))
+// computed once per qubit and symbol (the fp32 restatement's recipe; the
+// oracle's fp32 path uses the same factorisation, its fp64 path the
+// reference's literal per-edge form).
 template <int W, int T, bool ADD>
-__device__ __forceinline__ void vn_phase(const KParams &p, const uint8_t *vn_sym, const uint8_t *vn_deg,
-                                         float *msg, uint8_t *ehat, int tid)
+__device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, int tid)
 {
-    const int n = p.n, np_ = p.n_pad;
+    const int n = p.n;
+    const uint32_t rowb = (uint32_t)p.n_pad * 4;
     const float l0 = p.l0;
+    unsigned char *msg = gm.msg;
+#pragma unroll 1
     for (int j = tid; j < n; j += T) {
+        unsigned char *col = msg + 4 * j;
         if constexpr (W > 0) {
             constexpr int D = 2 * W;
             float c[D];
             OptF ox[D], oz[D], oa[D];
 #pragma unroll
             for (int s = 0; s < D; ++s) {
-                c[s] = msg[s * np_ + j];
-                // anti_Z keeps X-edges (x-bit), anti_X keeps Z-edges (z-bit)
+                c[s] = lds_f(col, s * rowb);
+                // anti_X keeps Z-edges (z-bit), anti_Z keeps X-edges (x-bit)
                 ox[s] = OptF{c[s], s >= W};
                 oz[s] = OptF{c[s], s < W};
                 oa[s] = OptF{c[s], true};
             }
-            const float totX = segsum_c<D>(ox);
-            const float totZ = segsum_c<D>(oz);
-            const float totY = segsum_c<D>(oa);
-            const float bX = l0 + totX, bZ = l0 + totZ;
-            ehat[j] = (uint8_t)hard_decision(bX, bZ, l0 + totY);
+            const float bX = l0 + segsum_c<D>(ox);
+            const float bZ = l0 + segsum_c<D>(oz);
+            const float tY = segsum_c<D>(oa);
+            const float bY = l0 + tY;
+            gm.ehat[j] = hard_decision(bX, bZ, bY);
             if constexpr (ADD) {
 #pragma unroll
-                for (int s = 0; s < D; ++s) msg[s * np_ + j] = clip64(l0 + (totY - c[s]));
+                for (int s = 0; s < D; ++s) sts_u(col, s * rowb, f2u(clip64(l0 + (tY - c[s]))));
             } else {
-                const float selfX = logaddexp(0.0f, -bX);
-                const float selfZ = logaddexp(0.0f, -bZ);
+                // X-edge: self X, anti {Z, Y}; Z-edge: self Z, anti {X, Y}
+                const float vX = logaddexp(0.0f, -bX) - logaddexp(-bZ, -bY);
+                const float vZ = logaddexp(0.0f, -bZ) - logaddexp(-bX, -bY);
 #pragma unroll
-                for (int s = 0; s < D; ++s) {
-                    // X-edge: b_a1 = b_Z, b_a2 = b_Y; Z-edge: b_a1 = b_X, b_a2 = b_Y
-                    const float ba1 = l0 + ((s < W ? totZ : totX) - c[s]);
-                    const float ba2 = l0 + (totY - c[s]);
-                    const float out = (s < W ? selfX : selfZ) - logaddexp(-ba1, -ba2);
-                    msg[s * np_ + j] = clip64(out);
-                }
+                for (int s = 0; s < D; ++s)
+                    sts_u(col, s * rowb, f2u(clip64((s < W ? vX : vZ) - c[s])));
             }
         } else {
-            const int d = vn_deg[j];
+            const int d = gm.vn_deg[j];
             float c[kGenericMaxDeg], tmp[kGenericMaxDeg];
             uint32_t sym[kGenericMaxDeg];
             for (int s = 0; s < d; ++s) {
-                c[s] = msg[s * np_ + j];
-                sym[s] = vn_sym[s * np_ + j];
+                c[s] = lds_f(col, s * rowb);
+                sym[s] = gm.vn_sym[s * p.n_pad + j];
             }
-            float tot[4];
+            float b[4];
 #pragma unroll
             for (int e = 1; e <= 3; ++e) {
                 for (int s = 0; s < d; ++s) {
@@ -374,92 +398,72 @@ __device__ __forceinline__ void vn_phase(const KParams &p, const uint8_t *vn_sym
                     const uint32_t a = e == 1 ? sz : (e == 2 ? sx : (sx ^ sz));
                     tmp[s] = a ? c[s] : 0.0f;
                 }
-                tot[e] = segsum_rt(tmp, d);
+                b[e] = l0 + segsum_rt(tmp, d);
             }
-            ehat[j] = (uint8_t)hard_decision(l0 + tot[1], l0 + tot[2], l0 + tot[3]);
+            gm.ehat[j] = hard_decision(b[1], b[2], b[3]);
             if constexpr (ADD) {
                 for (int s = 0; s < d; ++s) tmp[s] = c[s];
                 const float all = segsum_rt(tmp, d);
-                for (int s = 0; s < d; ++s) msg[s * np_ + j] = clip64(l0 + (all - c[s]));
+                for (int s = 0; s < d; ++s) sts_u(col, s * rowb, f2u(clip64(l0 + (all - c[s]))));
             } else {
-                for (int s = 0; s < d; ++s) {
-                    const uint32_t sx = sym[s] & 1u, sz = sym[s] >> 1;
-                    float b[4];
+                float V[4];
 #pragma unroll
-                    for (int e = 1; e <= 3; ++e) {
-                        const uint32_t a = e == 1 ? sz : (e == 2 ? sx : (sx ^ sz));
-                        b[e] = a ? l0 + (tot[e] - c[s]) : l0 + tot[e];
-                    }
-                    const float bs = sym[s] == 1 ? b[1] : (sym[s] == 3 ? b[3] : b[2]);
-                    const float b1 = sym[s] == 1 ? b[2] : b[1];
-                    const float b2 = sym[s] == 3 ? b[2] : b[3];
-                    msg[s * np_ + j] = clip64(logaddexp(0.0f, -bs) - logaddexp(-b1, -b2));
+                for (int S = 1; S <= 3; ++S) {
+                    const int a1 = S == 1 ? 2 : 1, a2 = S == 3 ? 2 : 3;
+                    V[S] = logaddexp(0.0f, -b[S]) - logaddexp(-b[a1], -b[a2]);
                 }
+                for (int s = 0; s < d; ++s) sts_u(col, s * rowb, f2u(clip64(V[sym[s]] - c[s])));
             }
         }
     }
 }
 
 template <int T>
-__device__ __forceinline__ void snapshot(const KParams &p, const float *msg, float *dst, int tid)
+__device__ __forceinline__ void snapshot(const KParams &p, const unsigned char *msg, float *dst, int tid)
 {
     const int total = p.dv_max * p.n_pad;
     for (int s = tid; s < total; s += T) {
         const int e = p.slot_edge[s];
-        if (e >= 0) dst[e] = msg[s];
+        if (e >= 0) dst[e] = lds_f(msg, 4u * s);
     }
 }
 
 template <int W, int T, bool BP4, bool ADD>
-__global__ void __launch_bounds__(1024) decode_kernel(const KParams p)
+__global__ void __launch_bounds__(512) decode_kernel(const KParams p)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     // ---- per-CTA copy of the graph tables ----
     {
-        const uint32_t words = p.tab_bytes / 4;
-        const uint32_t *src[5];
-        uint32_t sz[5];
-        const uint32_t tabw = (uint32_t)p.dc_max * p.m_pad / 2;
-        src[0] = (const uint32_t *)p.cn_slot; sz[0] = tabw;
-        int nsrc = 1;
+        uint32_t *dst = reinterpret_cast<uint32_t *>(smem);
+        const uint32_t tabw = (uint32_t)p.m_pad * p.row_words;
+        for (uint32_t w = threadIdx.x; w < tabw; w += blockDim.x) dst[w] = p.cn_tab[w];
         if constexpr (W == 0) {
-            src[1] = (const uint32_t *)p.cn_sym; sz[1] = (uint32_t)p.dc_max * p.m_pad / 4;
-            src[2] = (const uint32_t *)p.cn_deg; sz[2] = (uint32_t)p.m_pad / 4;
-            src[3] = (const uint32_t *)p.vn_sym; sz[3] = (uint32_t)p.dv_max * p.n_pad / 4;
-            src[4] = (const uint32_t *)p.vn_deg; sz[4] = (uint32_t)p.n_pad / 4;
-            nsrc = 5;
+            const uint32_t *vs = reinterpret_cast<const uint32_t *>(p.vn_sym);
+            const uint32_t *vd = reinterpret_cast<const uint32_t *>(p.vn_deg);
+            const uint32_t nsw = (uint32_t)p.dv_max * p.n_pad / 4, ndw = (uint32_t)p.n_pad / 4;
+            for (uint32_t w = threadIdx.x; w < nsw; w += blockDim.x) dst[tabw + w] = vs[w];
+            for (uint32_t w = threadIdx.x; w < ndw; w += blockDim.x) dst[tabw + nsw + w] = vd[w];
         }
-        uint32_t *dst = (uint32_t *)smem;
-        uint32_t off = 0;
-        for (int s = 0; s < nsrc; ++s) {
-            for (uint32_t w = threadIdx.x; w < sz[s]; w += blockDim.x) dst[off + w] = src[s][w];
-            off += sz[s];
-        }
-        (void)words;
     }
     __syncthreads();
-    const uint16_t *tab = (const uint16_t *)smem;
-    const uint8_t *cn_sym = nullptr, *cn_deg = nullptr, *vn_sym = nullptr, *vn_deg = nullptr;
-    if constexpr (W == 0) {
-        cn_sym = smem + (size_t)p.dc_max * p.m_pad * 2;
-        cn_deg = cn_sym + (size_t)p.dc_max * p.m_pad;
-        vn_sym = cn_deg + p.m_pad;
-        vn_deg = vn_sym + (size_t)p.dv_max * p.n_pad;
-    }
 
     const int g = threadIdx.x / T, tid = threadIdx.x % T;
     unsigned char *gbase = smem + p.tab_bytes + (size_t)g * p.group_bytes;
-    float *msg = (float *)gbase;
-    uint8_t *ehat = gbase + (size_t)p.dv_max * p.n_pad * 4;
-    int *scratch = (int *)(ehat + p.n_pad);  // 2*(T/32) ints + frame slot (2 ints)
-    long long *fslot = (long long *)(scratch + 2 * (T / 32) + ((2 * (T / 32)) & 1));
+    GroupMem gm;
+    gm.tab = reinterpret_cast<const uint32_t *>(smem);
+    gm.vn_sym = smem + (size_t)p.m_pad * p.row_words * 4;
+    gm.vn_deg = gm.vn_sym + (size_t)p.dv_max * p.n_pad;
+    gm.msg = gbase;
+    gm.ehat = reinterpret_cast<uint32_t *>(gbase + (size_t)p.dv_max * p.n_pad * 4);
+    int *scratch = reinterpret_cast<int *>(gm.ehat + p.n_pad);  // 2*(T/32) ints
+    long long *fslot = reinterpret_cast<long long *>(scratch + 2 * (T / 32));
 
     const int n = p.n, m = p.m, np_ = p.n_pad;
     const int msg_words = p.dv_max * np_;
     long long c_frames = 0, c_fail = 0, c_iters = 0;
 
     // hard decision with all-zero check messages: argmin(0, L0, L0, L0)
-    const uint8_t hd0 = (uint8_t)hard_decision(p.l0, p.l0, p.l0);
+    const uint32_t hd0 = hard_decision(p.l0, p.l0, p.l0);
     const bool capture = p.tr_vn != nullptr || p.tr_cn != nullptr;
 
     while (true) {
@@ -484,10 +488,10 @@ __global__ void __launch_bounds__(1024) decode_kernel(const KParams p)
                 const U64x4 w = philox4x64_10((uint64_t)b + 1, p.seed, key1);
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
-                    if (4 * b + q < n) ehat[4 * b + q] = pauli_from_word(w.v[q], p.kx, p.ky, p.kz);
+                    if (4 * b + q < n) gm.ehat[4 * b + q] = pauli_from_word(w.v[q], p.kx, p.ky, p.kz);
             }
             group_sync<T>(g);
-            syn_bits = syndrome_bits<W, T>(p, tab, cn_sym, cn_deg, ehat, tid);
+            syn_bits = syndrome_bits<W, T>(p, gm, tid);
             group_sync<T>(g);
         } else {
             syn_bits = 0;
@@ -495,13 +499,14 @@ __global__ void __launch_bounds__(1024) decode_kernel(const KParams p)
             const uint8_t *s_in = p.syn_in + f * (long long)m;
             for (int i = tid; i < m; i += T, ++t) syn_bits |= (s_in[i] != 0 ? 1u : 0u) << t;
         }
-        for (int j = tid; j < np_; j += T) ehat[j] = hd0;
-        for (int s = tid; s < msg_words; s += T) msg[s] = p.v0;
+        for (int j = tid; j < np_; j += T) gm.ehat[j] = hd0;
+        const uint32_t v0b = f2u(p.v0);
+        for (int s = tid; s < msg_words; s += T) sts_u(gm.msg, 4u * s, v0b);
         group_sync<T>(g);
 
         int recorded = 0, success = 0, iters = p.l_max, n_gamma = 0, n_snap = 0;
         for (int ell = 1; ell <= p.l_max; ++ell) {
-            const uint32_t res = syn_bits ^ syndrome_bits<W, T>(p, tab, cn_sym, cn_deg, ehat, tid);
+            const uint32_t res = syn_bits ^ syndrome_bits<W, T>(p, gm, tid);
             const int unsat = group_sum<T>(__popc(res), scratch, ell & 1, tid, g);
             if (p.tr_unsat && tid == 0) p.tr_unsat[f * p.l_max + n_gamma] = unsat;
             ++n_gamma;
@@ -510,12 +515,12 @@ __global__ void __launch_bounds__(1024) decode_kernel(const KParams p)
                 iters = ell;
                 recorded = 1;
                 if (p.out_ehat)
-                    for (int j = tid; j < n; j += T) p.out_ehat[f * n + j] = ehat[j];
+                    for (int j = tid; j < n; j += T) p.out_ehat[f * n + j] = (uint8_t)gm.ehat[j];
             }
             if (p.early_stop && unsat == 0) break;
             if (ell == p.l_max) {
                 if (!recorded && p.out_ehat)
-                    for (int j = tid; j < n; j += T) p.out_ehat[f * n + j] = ehat[j];
+                    for (int j = tid; j < n; j += T) p.out_ehat[f * n + j] = (uint8_t)gm.ehat[j];
                 if (!capture) break;
             }
             float g0 = 1.0f, g1 = 1.0f;
@@ -527,13 +532,13 @@ __global__ void __launch_bounds__(1024) decode_kernel(const KParams p)
                 g0 = (float)(base * 1.0);
                 g1 = (float)(base * p.eta);
             }
-            cn_phase<W, T, BP4>(p, tab, cn_deg, msg, syn_bits, res, g0, g1, tid);
+            cn_phase<W, T, BP4>(p, gm, syn_bits, res, g0, g1, tid);
             group_sync<T>(g);
-            if (capture && p.tr_cn) snapshot<T>(p, msg, p.tr_cn + (f * p.l_max + n_snap) * p.E, tid);
-            vn_phase<W, T, ADD>(p, vn_sym, vn_deg, msg, ehat, tid);
+            if (capture && p.tr_cn) snapshot<T>(p, gm.msg, p.tr_cn + (f * p.l_max + n_snap) * p.E, tid);
+            vn_phase<W, T, ADD>(p, gm, tid);
             group_sync<T>(g);
             if (capture) {
-                if (p.tr_vn) snapshot<T>(p, msg, p.tr_vn + (f * p.l_max + n_snap) * p.E, tid);
+                if (p.tr_vn) snapshot<T>(p, gm.msg, p.tr_vn + (f * p.l_max + n_snap) * p.E, tid);
                 ++n_snap;
             }
         }
