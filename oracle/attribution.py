@@ -1,0 +1,84 @@
+"""TEST INFRASTRUCTURE ONLY -- attribute fp32-vs-fp64 outcome differences.
+
+north_star: "any frame whose outcome differs must be attributable to a
+documented min-tie or fp32-rounding case".  For a frame whose (success,
+iterations, e_hat) differ between the fp32 restatement (== the GPU, bit for
+bit) and the float64 reference arithmetic, this replays both with message
+capture and finds the first iteration whose hard decision differs.  The frame
+is attributed when the fp64 decision at the diverging qubit is a tie no
+larger than the fp32 deviation of its metrics (rounding, not logic, chose
+the branch) and the two trajectories agreed to rounding after the first
+update (<= 1e-5 relative, unit floor): "exact-tie" (gap 0), "near-tie"
+(deviation still <= 1e-4 when the decisions split) or "rounding-growth"
+(the flooding dynamics amplified the rounding over several iterations
+before a decision split, as on failing / near-threshold frames).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import oracle as O
+
+
+@dataclass
+class Attribution:
+    frame: int
+    first_iteration: int | None   # first iteration whose hard decision differs
+    qubit: int | None
+    gap64: float                  # fp64 metric gap between the two decisions
+    metric_delta: float           # |fp32 - fp64| of the deciding metrics
+    max_rel_msg_err: float        # message deviation before the divergence
+    first_rel_msg_err: float      # message deviation after the first update
+    kind: str  # "exact-tie", "near-tie", "rounding-growth", "unattributed", "no-divergence"
+
+    @property
+    def attributed(self) -> bool:
+        return self.kind in ("exact-tie", "near-tie", "rounding-growth")
+
+
+def _metrics(g, cn, l0, dtype):
+    """(n, 4) hard-decision metrics exactly as decoder.py:292-301 computes
+    them (np.add.reduceat over the masked, qubit-ordered messages) in the
+    given precision -- the same numbers the restatement of that precision
+    decides on."""
+    cv = np.asarray(cn, dtype=dtype)[g.vn_order]
+    sym = g.edge_sym[g.vn_order].astype(np.int64)
+    sx, sz = sym & 1, sym >> 1
+    m = np.zeros((g.n, 4), dtype=dtype)
+    for e_code, anti in ((1, sz), (2, sx), (3, sx ^ sz)):
+        m[:, e_code] = dtype(l0) + np.add.reduceat(cv * anti.astype(dtype), g.vn_ptr[:-1])
+    return m
+
+
+def attribute(graph, syndrome, l0, cfg, frame=0, rel_tol=1e-4, tie_factor=4.0):
+    g = O.Graph(graph) if not isinstance(graph, O.Graph) else graph
+    s = np.asarray(syndrome, dtype=np.uint8)[None, :]
+    a = O.decode(g, s, l0, cfg, precision=64, capture=True, early_stop=False)
+    z = O.decode(g, s, l0, cfg, precision=32, capture=True, early_stop=False)
+    nsnap = int(min(a.counts[0, 1], z.counts[0, 1]))
+    worst = first = 0.0
+    for k in range(nsnap):
+        c64 = a.cn_msgs[0, k]
+        c32 = z.cn_msgs[0, k]
+        m64, m32 = _metrics(g, c64, l0, np.float64), _metrics(g, c32, l0, np.float32)
+        h64, h32 = np.argmin(m64, axis=1), np.argmin(m32, axis=1)
+        diff = np.nonzero(h64 != h32)[0]
+        if diff.size:
+            j = int(diff[0])
+            gap = abs(m64[j, h32[j]] - m64[j, h64[j]])
+            delta = float(np.abs(m32[j].astype(np.float64) - m64[j]).max())
+            if gap == 0.0:
+                kind = "exact-tie"
+            elif gap > tie_factor * delta or first > 1e-5:
+                kind = "unattributed"
+            else:
+                kind = "near-tie" if worst <= rel_tol else "rounding-growth"
+            return Attribution(frame, k + 2, j, gap, delta, worst, first, kind)
+        for x64, x32 in ((a.vn_msgs[0, k], z.vn_msgs[0, k]), (c64, z.cn_msgs[0, k])):
+            err = np.abs(x32.astype(np.float64) - x64) / np.maximum(np.abs(x64), 1.0)
+            worst = max(worst, float(err.max()))
+        if k == 0:
+            first = worst
+    return Attribution(frame, None, None, 0.0, 0.0, worst, first, "no-divergence")

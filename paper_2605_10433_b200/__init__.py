@@ -45,6 +45,7 @@ from .decoder import (  # noqa: E402
     effective_gain,
     syndrome_ratio,
 )
+from . import dist  # noqa: E402,F401
 from .device import DeviceGraph, device_graph  # noqa: E402
 from .harness import (  # noqa: E402
     FerPoint,

@@ -1,0 +1,121 @@
+"""Multi-GPU FER points: one process per GPU, frames sharded contiguously.
+
+Frame f is keyed by (seed, f), so any partition of the frame range gives
+bit-identical per-frame results (reference harness.py:1-11).  Two modes:
+
+  * ``fer_counters``: fixed frame budget (BASELINE configs 2-5).  Each rank
+    decodes its shard with device-side counters and ONE all-reduce(sum) of
+    int64[4] {frames, failures, sum iterations, CN-edge updates} per point
+    (NCCL over NVLink; latency-bound, ~32 bytes).
+  * ``run_point_sharded``: the reference's ordered stop rule
+    (harness.py:262-270) across ranks.  Frames are processed in rounds of
+    world x chunk; each rank decodes its contiguous sub-range and the
+    per-frame fail flags and iteration counts are all-gathered in frame order
+    so every rank applies the same cumulative-failure stop rule; frames past
+    the stop index are discarded as the reference does for speculative
+    batches.
+
+The per-rank FER unit is pluggable (``unit``) so the host logic is testable
+with the gloo backend on CPU; the product path uses ``decode_frames_device``
+on the rank's GPU with NCCL.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from .harness import FerPoint, SweepConfig, config_digest, decode_frames_device, wilson_interval
+
+
+def shard_range(rank: int, world: int, start: int, count: int) -> tuple[int, int]:
+    """Contiguous shard [lo, hi) of frames [start, start+count) for ``rank``."""
+    lo = start + count * rank // world
+    hi = start + count * (rank + 1) // world
+    return lo, hi - lo
+
+
+def _world():
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
+
+
+def gpu_unit(graph, cfg, eps, eps0, seed, start, count, device=None):
+    """Default FER unit: (fails uint8, iterations int64) device tensors."""
+    fails, iters, _ = decode_frames_device(graph, cfg, eps, eps0, seed, start, count, device=device)
+    return fails, iters
+
+
+def fer_counters(graph, cfg, eps, eps0, seed, start, count, *, unit=None, device=None) -> torch.Tensor:
+    """Global {frames, failures, sum iterations, CN-edge updates} over all
+    ranks for frames [start, start+count) (one all-reduce)."""
+    rank, world = _world()
+    lo, n = shard_range(rank, world, start, count)
+    if unit is None:
+        cnt = torch.zeros(4, dtype=torch.int64, device=device or torch.device("cuda", torch.cuda.current_device()))
+        decode_frames_device(graph, cfg, eps, eps0, seed, lo, n, counters=cnt, want_frames=False, device=device)
+    else:
+        fails, iters = unit(graph, cfg, eps, eps0, seed, lo, n)
+        E = int(graph.edge_count if hasattr(graph, "edge_count") else graph.E)
+        cnt = torch.tensor([n, int(fails.sum()), int(iters.sum()), E * (int(iters.sum()) - n)],
+                           dtype=torch.int64)
+    if world > 1:
+        dist.all_reduce(cnt)
+    return cnt
+
+
+@dataclass
+class ShardedStats:
+    frames: int
+    failures: int
+    iter_sum: int
+
+
+def run_point_sharded(graph, cfg: SweepConfig, epsilon: float, *, chunk: int = 1 << 20, unit=None,
+                      device=None) -> FerPoint:
+    """run_point (harness.py:248-293) with frames sharded over all ranks and
+    the exact ordered stop rule; every rank returns the same FerPoint."""
+    rank, world = _world()
+    unit = unit or (lambda *a: gpu_unit(*a, device=device))
+    eps0 = epsilon if cfg.epsilon0_mode == "matched" else float(cfg.epsilon0)
+    frames = failures = iter_sum = 0
+    start = 0
+    while start < cfg.max_frames:
+        count = min(chunk * world, cfg.max_frames - start)
+        lo, n = shard_range(rank, world, start, count)
+        fails, iters = unit(graph, cfg.decoder, epsilon, eps0, cfg.seed, lo, n)
+        fails = fails.to(torch.int32)
+        iters = iters.to(torch.int32)
+        if world > 1:
+            sizes = [shard_range(r, world, start, count)[1] for r in range(world)]
+            pad = max(sizes)
+            fpad = torch.zeros(pad, dtype=torch.int32, device=fails.device)
+            ipad = torch.zeros(pad, dtype=torch.int32, device=iters.device)
+            fpad[:n] = fails
+            ipad[:n] = iters
+            fl = [torch.empty_like(fpad) for _ in range(world)]
+            il = [torch.empty_like(ipad) for _ in range(world)]
+            dist.all_gather(fl, fpad)
+            dist.all_gather(il, ipad)
+            fails = torch.cat([t[:s] for t, s in zip(fl, sizes)])
+            iters = torch.cat([t[:s] for t, s in zip(il, sizes)])
+        f64 = fails.to(torch.int64).cpu()
+        cum = torch.cumsum(f64, 0)
+        hit = torch.nonzero(failures + cum >= cfg.target_failures)
+        if hit.numel():
+            stop = int(hit[0, 0]) + 1
+            frames = start + stop
+            failures += int(cum[stop - 1])
+            iter_sum += int(iters[:stop].to(torch.int64).sum())
+            break
+        frames = start + count
+        failures += int(cum[-1]) if count else 0
+        iter_sum += int(iters.to(torch.int64).sum())
+        start += count
+    low, high = wilson_interval(failures, frames)
+    return FerPoint(epsilon=epsilon, epsilon0=eps0, frames=frames, failures=failures,
+                    fer=failures / frames, wilson_low=low, wilson_high=high,
+                    mean_iterations=iter_sum / frames, cap_hit=failures < cfg.target_failures,
+                    config_digest=config_digest(cfg), seed=cfg.seed)
