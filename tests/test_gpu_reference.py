@@ -76,16 +76,21 @@ def test_gpu_outcomes_vs_reference_batches(P, oracle, cname, vn_mode, variant):
     # frames that differ from the float64 reference are exactly the frames
     # where the fp32 restatement differs from float64 arithmetic (each one
     # attributed on CPU); everywhere else the GPU reproduces the reference
-    r32 = oracle.decode(g, syn, P.prior_llr(float(eps)).llr, cfg, precision=32)
+    r32 = oracle.decode(g, syn, P.prior_llr(float(eps)).llr, cfg, precision=32, trace=True)
     assert np.array_equal(got.success, r32.success) and np.array_equal(got.iterations, r32.iterations)
-    r64 = oracle.decode(g, syn, P.prior_llr(float(eps)).llr, cfg, precision=64)
+    for a, c in zip(got.gamma_traces, r32.gamma_traces(g.m)):
+        assert np.array_equal(a, c)
+    r64 = oracle.decode(g, syn, P.prior_llr(float(eps)).llr, cfg, precision=64, trace=True)
     diff64 = (r32.success != r64.success) | (r32.iterations != r64.iterations) | (r32.e_hat != r64.e_hat).any(axis=1)
     if variant != "bp4":
         assert np.array_equal(~same, diff64)
-    lens = b[key + "/gamma_len"]
-    gam = np.split(b[key + "/gamma"], np.cumsum(lens)[:-1])
-    for f in np.nonzero(same)[0]:
-        assert np.array_equal(got.gamma_traces[f], gam[f])
+        # where fp32 and fp64 trajectories coincide, the GPU's gamma traces
+        # are the reference's
+        lens = b[key + "/gamma_len"]
+        gam = np.split(b[key + "/gamma"], np.cumsum(lens)[:-1])
+        for f, (t32, t64) in enumerate(zip(r32.gamma_traces(g.m), r64.gamma_traces(g.m))):
+            if np.array_equal(t32, t64):
+                assert np.array_equal(got.gamma_traces[f], gam[f])
 
 
 def test_config1_on_gpu_matches_reference_golden(P):
