@@ -73,6 +73,33 @@ bool bicycle_w_supported(int w)
     return false;
 }
 
+// Rows of build_gb (code.py:201-231) as canonical CSR: rows 0..ell-1 are X
+// on [A|B] (columns (i + a_k), ell + (i + b_k)), rows ell..2ell-1 are Z on
+// [B^T|A^T] (columns (i - b_k), ell + (i - a_k)), each row sorted.
+void gb_rows(int32_t ell, const int32_t *a, int32_t wa, const int32_t *b, int32_t wb,
+             std::vector<int64_t> &cn_ptr, std::vector<int64_t> &edge_vn, std::vector<uint8_t> &edge_sym)
+{
+    auto circ = [&](const int32_t *x, int w, int row, int sign) {
+        std::vector<int64_t> cols(w);
+        for (int k = 0; k < w; ++k) cols[k] = (((int64_t)row + sign * (int64_t)x[k]) % ell + ell) % ell;
+        std::sort(cols.begin(), cols.end());
+        return cols;
+    };
+    cn_ptr.assign(1, 0);
+    edge_vn.clear();
+    edge_sym.clear();
+    for (int i = 0; i < ell; ++i) {
+        for (int64_t c : circ(a, wa, i, 1)) { edge_vn.push_back(c); edge_sym.push_back(1); }
+        for (int64_t c : circ(b, wb, i, 1)) { edge_vn.push_back(ell + c); edge_sym.push_back(1); }
+        cn_ptr.push_back((int64_t)edge_vn.size());
+    }
+    for (int i = 0; i < ell; ++i) {
+        for (int64_t c : circ(b, wb, i, -1)) { edge_vn.push_back(c); edge_sym.push_back(2); }
+        for (int64_t c : circ(a, wa, i, -1)) { edge_vn.push_back(ell + c); edge_sym.push_back(2); }
+        cn_ptr.push_back((int64_t)edge_vn.size());
+    }
+}
+
 // ---- layout compiler ---------------------------------------------------------
 // Input: canonical CSR (TannerGraph order, code.py:150-191).  Output: the
 // TannerGraph arrays (kept for export), the qubit-major slot layout
@@ -130,22 +157,46 @@ int compile_layout(qsg_graph *g, int32_t n, int32_t m, const int64_t *cn_ptr, co
     while ((1 << g->log2_npad) < g->n_pad) ++g->log2_npad;
     g->m_pad = (m + 31) / 32 * 32;
 
-    // kernel kind
+    // kernel kind: generalized-bicycle circulant codes (code.py:201-231) with
+    // |a| = |b| = W get the specialised kernels; everything else the generic
+    // table-driven ones.
     int kind = 0;
-    if (dv_max % 2 == 0 && bicycle_w_supported(dv_max / 2) && (int64_t)dv_max * g->n_pad * 4 < (1 << 24)) {
-        const int W = dv_max / 2;
-        bool ok = true;
-        for (int i = 0; i < m && ok; ++i) {
-            ok = (cn_ptr[i + 1] - cn_ptr[i]) == 2 * W;
-            for (int64_t e = cn_ptr[i]; e < cn_ptr[i + 1] && ok; ++e) ok = edge_sym[e] == edge_sym[cn_ptr[i]];
-            ok = ok && (edge_sym[cn_ptr[i]] == 1 || edge_sym[cn_ptr[i]] == 2);
+    if (n % 2 == 0 && m == n && n / 2 >= 32 && dv_max % 2 == 0 && bicycle_w_supported(dv_max / 2) &&
+        (int64_t)dv_max * g->n_pad * 4 < (1 << 24)) {
+        const int32_t ell = n / 2, W = dv_max / 2;
+        std::vector<int32_t> a, b;
+        for (int64_t e = cn_ptr[0]; e < cn_ptr[1]; ++e)
+            (edge_vn[e] < ell ? a : b).push_back((int32_t)(edge_vn[e] < ell ? edge_vn[e] : edge_vn[e] - ell));
+        if ((int)a.size() == W && (int)b.size() == W) {
+            std::vector<int64_t> cp, ev;
+            std::vector<uint8_t> es;
+            gb_rows(ell, a.data(), W, b.data(), W, cp, ev, es);
+            bool same = (int64_t)ev.size() == E;
+            for (int i = 0; same && i <= m; ++i) same = cp[i] == cn_ptr[i];
+            for (int64_t e = 0; same && e < E; ++e) same = ev[e] == edge_vn[e] && es[e] == edge_sym[e];
+            if (same) {
+                kind = W;
+                g->ell = ell;
+                for (int k = 0; k < W; ++k) { g->gb_a[k] = a[k]; g->gb_b[k] = b[k]; }
+            }
         }
-        for (int j = 0; j < n && ok; ++j) {
-            ok = vdeg[j] == 2 * W;
-            for (int s = 0; s < 2 * W && ok; ++s)
-                ok = edge_sym[g->vn_order[g->vn_ptr[j] + s]] == (s < W ? 1 : 2);
+    }
+    // threads per frame: every thread owns <= 32 checks (register bit masks);
+    // bicycle kernels own circulant indices (at most 4 per thread)
+    const int nodes = std::max(n, m);
+    if (nodes <= 32 * 12) g->threads = 32;
+    else if (m <= 128 * 32) g->threads = 128;
+    else return fail(QSG_EUNSUPPORTED, "more than 4096 checks");
+    if (kind > 0) {
+        g->nw = (g->ell + 31) / 32;
+        const int lpw = g->threads / (2 * g->nw);  // lanes per syndrome word
+        if (lpw < 1) {
+            kind = 0;
+        } else {
+            int p2 = 1;
+            while (p2 * 2 <= lpw && p2 * 2 <= 32) p2 *= 2;
+            g->lpw = p2;
         }
-        if (ok) kind = W;
     }
     g->kind = kind;
     if (kind == 0) {
@@ -154,11 +205,6 @@ int compile_layout(qsg_graph *g, int32_t n, int32_t m, const int64_t *cn_ptr, co
         if ((int64_t)dv_max * g->n_pad * 4 >= (1 << 24))
             return fail(QSG_EUNSUPPORTED, "graph too large for 24-bit slot offsets");
     }
-    // threads per frame: every thread owns <= 32 checks (register bit masks)
-    const int nodes = std::max(n, m);
-    if (nodes <= 32 * 12) g->threads = 32;
-    else if (m <= 128 * 32) g->threads = 128;
-    else return fail(QSG_EUNSUPPORTED, "more than 4096 checks");
 
     // check table: one row of row_words (odd) u32 per check: byte offsets of
     // the check's edges in canonical order (generic rows also carry the edge
@@ -203,10 +249,17 @@ int compile_layout(qsg_graph *g, int32_t n, int32_t m, const int64_t *cn_ptr, co
     // shared-memory footprint
     size_t tab = (size_t)mp * rw * 4;
     if (kind == 0) tab += (size_t)dv_max * np_ + np_;
+    if (kind > 0) tab += 16 * 4;  // circulant exponents
     g->tab_bytes = (uint32_t)((tab + 15) / 16 * 16);
     const int T = g->threads;
-    size_t grp = (size_t)dv_max * np_ * 4 + (size_t)np_ * 4 + 2 * (T / 32) * 4 + 8;
-    g->group_bytes = (uint32_t)((grp + 15) / 16 * 16);
+    size_t off = (size_t)dv_max * np_ * 4;             // messages
+    g->off_ehat = (uint32_t)off; off += (size_t)np_ * 4;
+    g->off_bits = (uint32_t)off; off += (size_t)16 * (g->nw + 1);
+    g->off_synw = (uint32_t)off; off += (size_t)8 * g->nw;
+    g->off_resw = (uint32_t)off; off += (size_t)8 * g->nw;
+    off = (off + 7) / 8 * 8;
+    g->off_scratch = (uint32_t)off; off += 2 * (T / 32) * 4 + 8;
+    g->group_bytes = (uint32_t)((off + 15) / 16 * 16);
     return QSG_OK;
 }
 
@@ -293,6 +346,10 @@ void fill_graph_params(const qsg_graph *g, qsg::KParams &p)
     p.vn_sym = g->d_vn_sym; p.vn_deg = g->d_vn_deg; p.slot_edge = g->d_slot_edge;
     p.n = g->n; p.m = g->m; p.n_pad = g->n_pad; p.log2_npad = g->log2_npad; p.m_pad = g->m_pad;
     p.dc_max = g->dc_max; p.dv_max = g->dv_max; p.row_words = g->row_words; p.E = g->E;
+    p.ell = g->ell; p.nw = g->nw; p.lpw = g->lpw;
+    for (int k = 0; k < 8; ++k) { p.gb_a[k] = g->gb_a[k]; p.gb_b[k] = g->gb_b[k]; }
+    p.off_ehat = g->off_ehat; p.off_bits = g->off_bits; p.off_synw = g->off_synw;
+    p.off_resw = g->off_resw; p.off_scratch = g->off_scratch;
     p.tab_bytes = g->tab_bytes; p.group_bytes = g->group_bytes;
 }
 
@@ -423,26 +480,10 @@ int qsg_graph_create_gb(int32_t ell, const int32_t *a, int32_t wa, const int32_t
                 if (x[k] == x[i]) return fail(QSG_EINVAL, "duplicate exponent");
         }
     }
-    // build_gb (code.py:201-231): sorted circulant supports per row
-    auto circ = [&](const int32_t *x, int w, int row, int sign) {
-        std::vector<int64_t> cols(w);
-        for (int k = 0; k < w; ++k) cols[k] = (((int64_t)row + sign * (int64_t)x[k]) % ell + ell) % ell;
-        std::sort(cols.begin(), cols.end());
-        return cols;
-    };
     const int32_t m = 2 * ell, n = 2 * ell;
-    std::vector<int64_t> cn_ptr(1, 0), edge_vn;
+    std::vector<int64_t> cn_ptr, edge_vn;
     std::vector<uint8_t> edge_sym;
-    for (int i = 0; i < ell; ++i) {
-        for (int64_t c : circ(a, wa, i, 1)) { edge_vn.push_back(c); edge_sym.push_back(1); }
-        for (int64_t c : circ(b, wb, i, 1)) { edge_vn.push_back(ell + c); edge_sym.push_back(1); }
-        cn_ptr.push_back((int64_t)edge_vn.size());
-    }
-    for (int i = 0; i < ell; ++i) {
-        for (int64_t c : circ(b, wb, i, -1)) { edge_vn.push_back(c); edge_sym.push_back(2); }
-        for (int64_t c : circ(a, wa, i, -1)) { edge_vn.push_back(ell + c); edge_sym.push_back(2); }
-        cn_ptr.push_back((int64_t)edge_vn.size());
-    }
+    gb_rows(ell, a, wa, b, wb, cn_ptr, edge_vn, edge_sym);
     return qsg_graph_create_csr(n, m, cn_ptr.data(), edge_vn.data(), edge_sym.data(), device, out);
 }
 

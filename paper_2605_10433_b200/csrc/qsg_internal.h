@@ -43,6 +43,8 @@ struct qsg_graph {
     int64_t E = 0;
     int32_t dc_max = 0, dv_max = 0, kind = 0, threads = 32;
     int32_t n_pad = 0, log2_npad = 0, m_pad = 0, row_words = 0;
+    int32_t ell = 0, nw = 0, lpw = 0, gb_a[8] = {0}, gb_b[8] = {0};  // bicycle kernels
+    uint32_t off_ehat = 0, off_bits = 0, off_synw = 0, off_resw = 0, off_scratch = 0;
     int32_t num_sms = 0;
     // canonical TannerGraph arrays (host)
     std::vector<int64_t> edge_cn, edge_vn, cn_ptr, vn_order, vn_ptr;

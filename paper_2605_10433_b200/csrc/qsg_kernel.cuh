@@ -24,10 +24,14 @@
 // entries 0..d-1 in canonical order (the order of the BP4 phi sum) and an
 // info word at index dc_max.  Hard decisions are kept as one u32 per qubit.
 //
-// W > 0 selects the "bicycle" specialisation (all degrees 2W, each qubit's
-// edges X-then-Z, single-symbol checks: every GB code with |a| = |b| = W),
-// in which degrees, masks and numpy's pairwise summation tree are compile
-// time constants.  W == 0 is the generic table-driven path (any graph).
+// W > 0 selects the generalized-bicycle specialisation (circulant A, B with
+// |a| = |b| = W, code.py:201-231): degrees, masks and numpy's pairwise
+// summation tree are compile-time constants, thread t owns circulant index c
+// (check c, check l+c, qubit c, qubit l+c), and the residual syndrome is
+// computed bit-sliced -- hard decisions are ballot-packed into four l-bit
+// circulant bitmaps (x/z bits of each block) and every 32-check syndrome
+// word is the XOR of 2W rotated 32-bit windows of them.  W == 0 is the
+// generic table-driven path (any graph).
 #pragma once
 
 #include <stdint.h>
@@ -47,6 +51,9 @@ struct KParams {
     const int32_t *slot_edge;  // [dv_max*n_pad]  canonical edge per slot (traces)
     int32_t n, m, n_pad, log2_npad, m_pad, dc_max, dv_max, row_words;
     int64_t E;
+    // generalized-bicycle circulant description (W > 0 kernels)
+    int32_t ell, nw, lpw;       // circulant size, 32-bit words per block, lanes per word
+    int32_t gb_a[8], gb_b[8];   // exponents of a(x), b(x)
     // decoder
     int32_t gain_mode;  // 0: none (bp4/ms), 1: constant alpha (sms), 2: sagms
     int32_t l_max, early_stop;
@@ -69,9 +76,10 @@ struct KParams {
     int32_t *tr_unsat;
     float *tr_vn, *tr_cn;
     int32_t *tr_counts;
-    // layout
+    // layout (byte offsets inside one group's shared-memory area)
     int32_t groups;  // groups per CTA
-    uint32_t tab_bytes, group_bytes, syn_words;
+    uint32_t tab_bytes, group_bytes;
+    uint32_t off_ehat, off_bits, off_synw, off_resw, off_scratch;
 };
 
 // ---- optional-value arithmetic for compile-time masked reductions ---------
@@ -190,9 +198,15 @@ struct GroupMem {
     const uint32_t *tab;     // check rows (byte offsets into msg)
     const uint8_t *vn_sym;   // generic only
     const uint8_t *vn_deg;   // generic only
+    const int32_t *gbexp;    // bicycle: a exponents [0, 8), b exponents [8, 16)
     unsigned char *msg;      // fp32 messages, slot-major
-    uint32_t *ehat;          // one Pauli code per qubit
+    uint32_t *ehat;          // generic: one Pauli code per qubit; bicycle: byte scratch
+    uint32_t *bits;          // bicycle: XL, ZL, XR, ZR circulant bitmaps, nw+1 words each
+    uint32_t *synw;          // bicycle: observed syndrome words (X checks, then Z checks)
+    uint32_t *resw;          // bicycle: residual syndrome words
 };
+
+enum { kXL = 0, kZL = 1, kXR = 2, kZR = 3 };
 
 __device__ __forceinline__ float lds_f(const unsigned char *base, uint32_t off)
 {
@@ -203,12 +217,10 @@ __device__ __forceinline__ void sts_u(unsigned char *base, uint32_t off, uint32_
     *reinterpret_cast<uint32_t *>(base + off) = v;
 }
 
-// Residual (or syndrome) bits of this thread's checks; bit t <-> check
-// tid + t*T.  gm.ehat holds one Pauli code per qubit.  For a check with
-// single symbol S the parity of trace(e_j, S) is one bit of the XOR of the
-// codes (z-bit for X checks, x-bit for Z checks), decoder.py:303-309.
-template <int W, int T>
-__device__ __forceinline__ uint32_t syndrome_bits(const KParams &p, const GroupMem &gm, int tid)
+// ---- generic residual (table-driven, decoder.py:303-309) -------------------
+// Bits of this thread's checks; bit t <-> check tid + t*T.
+template <int T>
+__device__ __forceinline__ uint32_t syndrome_bits_generic(const KParams &p, const GroupMem &gm, int tid)
 {
     uint32_t bits = 0;
     const uint32_t jmask = (uint32_t)(p.n_pad - 1) << 2;
@@ -218,23 +230,96 @@ __device__ __forceinline__ uint32_t syndrome_bits(const KParams &p, const GroupM
     for (int i = tid; i < p.m; i += T, ++t) {
         const uint32_t *row = gm.tab + i * p.row_words;
         uint32_t x = 0;
-        if constexpr (W > 0) {
-#pragma unroll
-            for (int k = 0; k < 2 * W; ++k)
-                x ^= *reinterpret_cast<const uint32_t *>(eb + (row[k] & jmask));
-            x >>= row[p.dc_max];  // info word: 1 for X checks, 0 for Z checks
-        } else {
-            const int d = (int)row[p.dc_max];
-            for (int k = 0; k < d; ++k) {
-                const uint32_t ent = row[k];
-                const uint32_t c = *reinterpret_cast<const uint32_t *>(eb + (ent & jmask));
-                const uint32_t sym = ent >> 30;
-                x ^= ((c & 1u) & (sym >> 1)) ^ ((c >> 1) & (sym & 1u));
-            }
+        const int d = (int)row[p.dc_max];
+        for (int k = 0; k < d; ++k) {
+            const uint32_t ent = row[k];
+            const uint32_t c = *reinterpret_cast<const uint32_t *>(eb + (ent & jmask));
+            const uint32_t sym = ent >> 30;
+            x ^= ((c & 1u) & (sym >> 1)) ^ ((c >> 1) & (sym & 1u));
         }
         bits |= (x & 1u) << t;
     }
     return bits;
+}
+
+// ---- bit-sliced circulant syndrome (bicycle kernels) -----------------------
+// Bits start..start+31 (indices mod l) of an l-bit circular bitmap B whose
+// bits >= l are zero and which has one zero padding word (l >= 32).
+__device__ __forceinline__ uint32_t circ_window(const uint32_t *B, int l, int start)
+{
+    const int q = start >> 5;
+    uint32_t w = __funnelshift_r(B[q], B[q + 1], start & 31);
+    const int n1 = l - start;
+    if (n1 < 32) w |= B[0] << n1;
+    return w;
+}
+
+// Syndrome words of the error held in the bitmaps (decoder.py:303-309 for
+// the GB rows of code.py:216-223): X check c has parity
+//   XOR_k z_L[c + a_k] ^ XOR_k z_R[c + b_k]          (indices mod l)
+// and Z check l+c
+//   XOR_k x_L[c - b_k] ^ XOR_k x_R[c - a_k].
+// Word w < nw holds X checks 32w..32w+31, word nw + w the Z checks; T/(2 nw)
+// lanes cooperate on a word and XOR-reduce with shuffles.  Writes
+// out[w] = base[w] ^ parity (base may be null) and returns this thread's
+// share of popc(out) (for the unsat count).
+template <int W, int T>
+__device__ __forceinline__ int circ_syndrome(const KParams &p, const GroupMem &gm, const uint32_t *base,
+                                             uint32_t *out, int tid)
+{
+    const int nw = p.nw, l = p.ell;
+    const int lpw = p.lpw;  // lanes per syndrome word (power of two <= 32, host-computed)
+    const int w = tid / lpw, sub = tid - w * lpw;
+    uint32_t acc = 0;
+    bool zc = false;
+    int ww = 0;
+    if (w < 2 * nw) {
+        zc = w >= nw;
+        ww = zc ? w - nw : w;
+        const uint32_t *BL = gm.bits + (zc ? kXL : kZL) * (nw + 1);
+        const uint32_t *BR = gm.bits + (zc ? kXR : kZR) * (nw + 1);
+        for (int k = sub; k < 2 * W; k += lpw) {
+            const bool left = k < W;
+            // X: left a_k, right b_k; Z: left -b_k, right -a_k
+            const int e = gm.gbexp[(left != zc) ? k % W : 8 + k % W];
+            int start = 32 * ww + (zc ? l - e : e);
+            start = start >= l ? start - l : start;
+            start = start >= l ? start - l : start;
+            acc ^= circ_window(left ? BL : BR, l, start);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        if (o < lpw) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
+    int cnt = 0;
+    if (w < 2 * nw && sub == 0) {
+        const int valid = l - 32 * ww;
+        const uint32_t mask = valid >= 32 ? 0xffffffffu : ((1u << valid) - 1u);
+        const uint32_t v = ((base ? base[w] : 0u) ^ acc) & mask;
+        out[w] = v;
+        cnt = __popc(v);
+    }
+    return cnt;
+}
+
+// Pack per-qubit Pauli codes (bytes in gm.ehat scratch) into the bitmaps.
+template <int T>
+__device__ __forceinline__ void bitmaps_from_bytes(const KParams &p, const GroupMem &gm, int tid)
+{
+    const int l = p.ell;
+    const uint8_t *e = reinterpret_cast<const uint8_t *>(gm.ehat);
+    const int nw1 = p.nw + 1;
+    for (int c0 = tid & ~31; c0 < 32 * p.nw; c0 += T) {
+        const int c = c0 + (tid & 31);
+        const uint32_t eL = c < l ? e[c] : 0u, eR = c < l ? e[l + c] : 0u;
+        const uint32_t xl = __ballot_sync(0xffffffffu, eL & 1u), zl = __ballot_sync(0xffffffffu, eL >> 1);
+        const uint32_t xr = __ballot_sync(0xffffffffu, eR & 1u), zr = __ballot_sync(0xffffffffu, eR >> 1);
+        if ((tid & 31) == 0) {
+            const int wd = c0 >> 5;
+            gm.bits[kXL * nw1 + wd] = xl; gm.bits[kZL * nw1 + wd] = zl;
+            gm.bits[kXR * nw1 + wd] = xr; gm.bits[kZR * nw1 + wd] = zr;
+        }
+    }
 }
 
 // ---- check-node phase (decoder.py:311-338) ---------------------------------
@@ -243,62 +328,105 @@ __device__ __forceinline__ uint32_t syndrome_bits(const KParams &p, const GroupM
 // the first-argmin rule (:325-333) without tracking the index.  Signs: the
 // extrinsic sign is (-1)^s_i * prod(sgn) * sgn_e (:314-316); messages are
 // never -0.0, so sgn_e is the IEEE sign bit and the product is an XOR.
+template <int D, bool BP4>
+__device__ __forceinline__ void cn_update_fixed(const uint32_t *row, unsigned char *msg, uint32_t sneg, float gain)
+{
+    uint32_t off[D];
+    float v[D];
+    uint32_t sx = sneg;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        off[k] = row[k];
+        v[k] = lds_f(msg, off[k]);
+        sx ^= f2u(v[k]);
+    }
+    const uint32_t sgn = sx & 0x80000000u;  // (-1)^s_i * prod sgn, as a sign bit
+    if constexpr (BP4) {
+        float ph[D];
+        OptF o[D];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            ph[k] = phi(fmaxf(fabsf(v[k]), 1e-12f));
+            o[k] = OptF{ph[k], true};
+        }
+        const float total = segsum_c<D>(o);
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            const float ext = fminf(fmaxf(total - ph[k], 1e-12f), 50.0f);
+            const uint32_t mag = f2u(fminf(phi(ext), kClip)) ^ sgn;
+            sts_u(msg, off[k], (f2u(v[k]) & 0x80000000u) ^ mag);
+        }
+    } else {
+        // smallest and second smallest of |v| (with multiplicity), two at a
+        // time: second' = min(second, max(min1, lo), hi)
+        float mn1, mn2;
+        {
+            const float a = fabsf(v[0]), b = fabsf(v[1]);
+            mn1 = fminf(a, b);
+            mn2 = fmaxf(a, b);
+        }
+#pragma unroll
+        for (int k = 2; k + 1 < D; k += 2) {
+            const float a = fabsf(v[k]), b = fabsf(v[k + 1]);
+            const float lo = fminf(a, b), hi = fmaxf(a, b);
+            mn2 = fminf(fminf(mn2, fmaxf(mn1, lo)), hi);
+            mn1 = fminf(mn1, lo);
+        }
+        if constexpr (D % 2) {
+            const float a = fabsf(v[D - 1]);
+            mn2 = fminf(mn2, fmaxf(mn1, a));
+            mn1 = fminf(mn1, a);
+        }
+        const uint32_t m1 = f2u(fminf(gain * mn1, kClip)) ^ sgn;
+        const uint32_t m2 = f2u(fminf(gain * mn2, kClip)) ^ sgn;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            const uint32_t mag = fabsf(v[k]) == mn1 ? m2 : m1;
+            sts_u(msg, off[k], (f2u(v[k]) & 0x80000000u) ^ mag);
+        }
+    }
+}
+
+// Inline both circulant halves (check c and l + c, qubit c and l + c) only
+// where the extra code still fits the instruction cache: the min-sum
+// kernels with one warp per frame.  BP4 (20 inlined phi per check) and the
+// 128-thread kernels measured faster with a single copy in a loop.
+template <int T, bool BP4>
+constexpr bool kUnrollPair = T == 32 && !BP4;
+
 template <int W, int T, bool BP4>
 __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, uint32_t syn_bits,
                                          uint32_t res_bits, float g0, float g1, int tid)
 {
-    constexpr uint32_t kAddr = 0x00ffffffu;  // generic entries carry sym << 30
     unsigned char *msg = gm.msg;
-    int t = 0;
+    if constexpr (W > 0) {
+        const int l = p.ell, nw = p.nw;
 #pragma unroll 1
-    for (int i = tid; i < p.m; i += T, ++t) {
-        const uint32_t *row = gm.tab + i * p.row_words;
-        const uint32_t sneg = ((syn_bits >> t) & 1u) << 31;
-        const float gain = ((res_bits >> t) & 1u) ? g1 : g0;
-        if constexpr (W > 0) {
-            constexpr int D = 2 * W;
-            uint32_t off[D];
-            float v[D];
-            uint32_t sx = sneg;
-#pragma unroll
-            for (int k = 0; k < D; ++k) {
-                off[k] = row[k];
-                v[k] = lds_f(msg, off[k]);
-                sx ^= f2u(v[k]);
-            }
-            const uint32_t sgn = sx & 0x80000000u;  // (-1)^s_i * prod sgn, as a sign bit
-            if constexpr (BP4) {
-                float ph[D];
-                OptF o[D];
-#pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    ph[k] = phi(fmaxf(fabsf(v[k]), 1e-12f));
-                    o[k] = OptF{ph[k], true};
-                }
-                const float total = segsum_c<D>(o);
-#pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    const float ext = fminf(fmaxf(total - ph[k], 1e-12f), 50.0f);
-                    const uint32_t mag = f2u(fminf(phi(ext), kClip)) ^ sgn;
-                    sts_u(msg, off[k], (f2u(v[k]) & 0x80000000u) ^ mag);
-                }
+        for (int c = tid; c < l; c += T) {
+            const int bit = c & 31;
+            // X check c (h = 0), Z check l + c (h = 1)
+            auto one = [&](int h) {
+                const int wd = h * nw + (c >> 5);
+                const uint32_t sy = gm.synw[wd] >> bit, rs = gm.resw[wd] >> bit;
+                cn_update_fixed<2 * W, BP4>(gm.tab + (h * l + c) * p.row_words, msg, sy << 31,
+                                            (rs & 1u) ? g1 : g0);
+            };
+            if constexpr (kUnrollPair<T, BP4>) {
+                one(0);
+                one(1);
             } else {
-                float mn1 = fabsf(v[0]), mn2 = __int_as_float(0x7f800000);
-#pragma unroll
-                for (int k = 1; k < D; ++k) {
-                    const float a = fabsf(v[k]);
-                    mn2 = fminf(mn2, fmaxf(mn1, a));
-                    mn1 = fminf(mn1, a);
-                }
-                const uint32_t m1 = f2u(fminf(gain * mn1, kClip)) ^ sgn;
-                const uint32_t m2 = f2u(fminf(gain * mn2, kClip)) ^ sgn;
-#pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    const uint32_t mag = fabsf(v[k]) == mn1 ? m2 : m1;
-                    sts_u(msg, off[k], (f2u(v[k]) & 0x80000000u) ^ mag);
-                }
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h) one(h);
             }
-        } else {
+        }
+    } else {
+        constexpr uint32_t kAddr = 0x00ffffffu;  // generic entries carry sym << 30
+        int t = 0;
+#pragma unroll 1
+        for (int i = tid; i < p.m; i += T, ++t) {
+            const uint32_t *row = gm.tab + i * p.row_words;
+            const uint32_t sneg = ((syn_bits >> t) & 1u) << 31;
+            const float gain = ((res_bits >> t) & 1u) ? g1 : g0;
             const int d = (int)row[p.dc_max];
             uint32_t off[kGenericMaxDeg];
             float v[kGenericMaxDeg];
@@ -343,46 +471,74 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, u
 //   V[S] = LAE(0, -(l0 + tot_S)) - LAE(-(l0 + tot_a1), -(l0 + tot_a2))
 // computed once per qubit and symbol (the fp32 restatement's recipe; the
 // oracle's fp32 path uses the same factorisation, its fp64 path the
-// reference's literal per-edge form).
+// reference's literal per-edge form).  Returns the hard decision.
+template <int W, bool ADD>
+__device__ __forceinline__ uint32_t vn_update_fixed(unsigned char *col, uint32_t rowb, float l0)
+{
+    constexpr int D = 2 * W;
+    float c[D];
+    OptF ox[D], oz[D], oa[D];
+#pragma unroll
+    for (int s = 0; s < D; ++s) {
+        c[s] = lds_f(col, s * rowb);
+        // anti_X keeps Z-edges (z-bit), anti_Z keeps X-edges (x-bit)
+        ox[s] = OptF{c[s], s >= W};
+        oz[s] = OptF{c[s], s < W};
+        oa[s] = OptF{c[s], true};
+    }
+    const float bX = l0 + segsum_c<D>(ox);
+    const float bZ = l0 + segsum_c<D>(oz);
+    const float tY = segsum_c<D>(oa);
+    const float bY = l0 + tY;
+    if constexpr (ADD) {
+#pragma unroll
+        for (int s = 0; s < D; ++s) sts_u(col, s * rowb, f2u(clip64(l0 + (tY - c[s]))));
+    } else {
+        // X-edge: self X, anti {Z, Y}; Z-edge: self Z, anti {X, Y}
+        const float vX = logaddexp(0.0f, -bX) - logaddexp(-bZ, -bY);
+        const float vZ = logaddexp(0.0f, -bZ) - logaddexp(-bX, -bY);
+#pragma unroll
+        for (int s = 0; s < D; ++s) sts_u(col, s * rowb, f2u(clip64((s < W ? vX : vZ) - c[s])));
+    }
+    return hard_decision(bX, bZ, bY);
+}
+
 template <int W, int T, bool ADD>
 __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, int tid)
 {
-    const int n = p.n;
     const uint32_t rowb = (uint32_t)p.n_pad * 4;
     const float l0 = p.l0;
     unsigned char *msg = gm.msg;
+    if constexpr (W > 0) {
+        // thread owns qubits c and l + c; the warp ballots their hard
+        // decisions into word c >> 5 of the circulant bitmaps
+        const int l = p.ell, nw1 = p.nw + 1;
 #pragma unroll 1
-    for (int j = tid; j < n; j += T) {
-        unsigned char *col = msg + 4 * j;
-        if constexpr (W > 0) {
-            constexpr int D = 2 * W;
-            float c[D];
-            OptF ox[D], oz[D], oa[D];
-#pragma unroll
-            for (int s = 0; s < D; ++s) {
-                c[s] = lds_f(col, s * rowb);
-                // anti_X keeps Z-edges (z-bit), anti_Z keeps X-edges (x-bit)
-                ox[s] = OptF{c[s], s >= W};
-                oz[s] = OptF{c[s], s < W};
-                oa[s] = OptF{c[s], true};
+        for (int c0 = tid & ~31; c0 < l; c0 += T) {
+            const int c = c0 + (tid & 31);
+            uint32_t e2[2] = {0u, 0u};
+            if (c < l) {
+                if constexpr (kUnrollPair<T, false>) {
+                    e2[0] = vn_update_fixed<W, ADD>(msg + 4 * c, rowb, l0);
+                    e2[1] = vn_update_fixed<W, ADD>(msg + 4 * (l + c), rowb, l0);
+                } else {
+#pragma unroll 1
+                    for (int h = 0; h < 2; ++h) e2[h] = vn_update_fixed<W, ADD>(msg + 4 * (h * l + c), rowb, l0);
+                }
             }
-            const float bX = l0 + segsum_c<D>(ox);
-            const float bZ = l0 + segsum_c<D>(oz);
-            const float tY = segsum_c<D>(oa);
-            const float bY = l0 + tY;
-            gm.ehat[j] = hard_decision(bX, bZ, bY);
-            if constexpr (ADD) {
-#pragma unroll
-                for (int s = 0; s < D; ++s) sts_u(col, s * rowb, f2u(clip64(l0 + (tY - c[s]))));
-            } else {
-                // X-edge: self X, anti {Z, Y}; Z-edge: self Z, anti {X, Y}
-                const float vX = logaddexp(0.0f, -bX) - logaddexp(-bZ, -bY);
-                const float vZ = logaddexp(0.0f, -bZ) - logaddexp(-bX, -bY);
-#pragma unroll
-                for (int s = 0; s < D; ++s)
-                    sts_u(col, s * rowb, f2u(clip64((s < W ? vX : vZ) - c[s])));
+            const uint32_t eL = e2[0], eR = e2[1];
+            const uint32_t xl = __ballot_sync(0xffffffffu, eL & 1u), zl = __ballot_sync(0xffffffffu, eL >> 1);
+            const uint32_t xr = __ballot_sync(0xffffffffu, eR & 1u), zr = __ballot_sync(0xffffffffu, eR >> 1);
+            if ((tid & 31) == 0) {
+                const int wd = c0 >> 5;
+                gm.bits[kXL * nw1 + wd] = xl; gm.bits[kZL * nw1 + wd] = zl;
+                gm.bits[kXR * nw1 + wd] = xr; gm.bits[kZR * nw1 + wd] = zr;
             }
-        } else {
+        }
+    } else {
+#pragma unroll 1
+        for (int j = tid; j < p.n; j += T) {
+            unsigned char *col = msg + 4 * j;
             const int d = gm.vn_deg[j];
             float c[kGenericMaxDeg], tmp[kGenericMaxDeg];
             uint32_t sym[kGenericMaxDeg];
@@ -428,14 +584,30 @@ __device__ __forceinline__ void snapshot(const KParams &p, const unsigned char *
     }
 }
 
+// current hard decision of qubit j
+template <int W>
+__device__ __forceinline__ uint8_t ehat_of(const KParams &p, const GroupMem &gm, int j)
+{
+    if constexpr (W > 0) {
+        const int nw1 = p.nw + 1;
+        const bool right = j >= p.ell;
+        const int c = right ? j - p.ell : j;
+        const uint32_t x = gm.bits[(right ? kXR : kXL) * nw1 + (c >> 5)] >> (c & 31);
+        const uint32_t z = gm.bits[(right ? kZR : kZL) * nw1 + (c >> 5)] >> (c & 31);
+        return (uint8_t)((x & 1u) | ((z & 1u) << 1));
+    } else {
+        return (uint8_t)gm.ehat[j];
+    }
+}
+
 template <int W, int T, bool BP4, bool ADD>
 __global__ void __launch_bounds__(512) decode_kernel(const KParams p)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     // ---- per-CTA copy of the graph tables ----
+    const uint32_t tabw = (uint32_t)p.m_pad * p.row_words;
     {
         uint32_t *dst = reinterpret_cast<uint32_t *>(smem);
-        const uint32_t tabw = (uint32_t)p.m_pad * p.row_words;
         for (uint32_t w = threadIdx.x; w < tabw; w += blockDim.x) dst[w] = p.cn_tab[w];
         if constexpr (W == 0) {
             const uint32_t *vs = reinterpret_cast<const uint32_t *>(p.vn_sym);
@@ -443,6 +615,9 @@ __global__ void __launch_bounds__(512) decode_kernel(const KParams p)
             const uint32_t nsw = (uint32_t)p.dv_max * p.n_pad / 4, ndw = (uint32_t)p.n_pad / 4;
             for (uint32_t w = threadIdx.x; w < nsw; w += blockDim.x) dst[tabw + w] = vs[w];
             for (uint32_t w = threadIdx.x; w < ndw; w += blockDim.x) dst[tabw + nsw + w] = vd[w];
+        } else {
+            if (threadIdx.x < 16)
+                dst[tabw + threadIdx.x] = (uint32_t)(threadIdx.x < 8 ? p.gb_a[threadIdx.x] : p.gb_b[threadIdx.x - 8]);
         }
     }
     __syncthreads();
@@ -451,11 +626,15 @@ __global__ void __launch_bounds__(512) decode_kernel(const KParams p)
     unsigned char *gbase = smem + p.tab_bytes + (size_t)g * p.group_bytes;
     GroupMem gm;
     gm.tab = reinterpret_cast<const uint32_t *>(smem);
-    gm.vn_sym = smem + (size_t)p.m_pad * p.row_words * 4;
+    gm.vn_sym = smem + (size_t)tabw * 4;
     gm.vn_deg = gm.vn_sym + (size_t)p.dv_max * p.n_pad;
+    gm.gbexp = reinterpret_cast<const int32_t *>(smem + (size_t)tabw * 4);
     gm.msg = gbase;
-    gm.ehat = reinterpret_cast<uint32_t *>(gbase + (size_t)p.dv_max * p.n_pad * 4);
-    int *scratch = reinterpret_cast<int *>(gm.ehat + p.n_pad);  // 2*(T/32) ints
+    gm.ehat = reinterpret_cast<uint32_t *>(gbase + p.off_ehat);
+    gm.bits = reinterpret_cast<uint32_t *>(gbase + p.off_bits);
+    gm.synw = reinterpret_cast<uint32_t *>(gbase + p.off_synw);
+    gm.resw = reinterpret_cast<uint32_t *>(gbase + p.off_resw);
+    int *scratch = reinterpret_cast<int *>(gbase + p.off_scratch);  // 2*(T/32) ints
     long long *fslot = reinterpret_cast<long long *>(scratch + 2 * (T / 32));
 
     const int n = p.n, m = p.m, np_ = p.n_pad;
@@ -479,35 +658,80 @@ __global__ void __launch_bounds__(512) decode_kernel(const KParams p)
         }
         if (f >= p.count) break;
 
-        // ---- frame input: observed syndrome bits per owned check ----
-        uint32_t syn_bits;
-        if (p.sample) {
-            const uint64_t key1 = (uint64_t)(p.start + f);
-            const int nblk = (n + 3) >> 2;
-            for (int b = tid; b < nblk; b += T) {
-                const U64x4 w = philox4x64_10((uint64_t)b + 1, p.seed, key1);
+        // ---- frame input: observed syndrome ----
+        uint32_t syn_bits = 0;
+        if constexpr (W > 0) {
+            uint8_t *eb = reinterpret_cast<uint8_t *>(gm.ehat);
+            if (p.sample) {
+                const uint64_t key1 = (uint64_t)(p.start + f);
+                const int nblk = (n + 3) >> 2;
+                for (int b = tid; b < nblk; b += T) {
+                    const U64x4 w = philox4x64_10((uint64_t)b + 1, p.seed, key1);
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (4 * b + q < n) gm.ehat[4 * b + q] = pauli_from_word(w.v[q], p.kx, p.ky, p.kz);
+                    for (int q = 0; q < 4; ++q)
+                        if (4 * b + q < n) eb[4 * b + q] = pauli_from_word(w.v[q], p.kx, p.ky, p.kz);
+                }
+                for (int w = tid; w < 4 * (p.nw + 1); w += T) gm.bits[w] = 0u;
+                group_sync<T>(g);
+                bitmaps_from_bytes<T>(p, gm, tid);
+                group_sync<T>(g);
+                circ_syndrome<W, T>(p, gm, nullptr, gm.synw, tid);
+            } else {
+                // observed syndrome rows: X checks c < l, Z checks l + c
+                const uint8_t *s_in = p.syn_in + f * (long long)m;
+                const int l = p.ell;
+                for (int c0 = tid & ~31; c0 < 32 * p.nw; c0 += T) {
+                    const int c = c0 + (tid & 31);
+                    const uint32_t bx = __ballot_sync(0xffffffffu, c < l && s_in[c] != 0);
+                    const uint32_t bz = __ballot_sync(0xffffffffu, c < l && s_in[l + c] != 0);
+                    if ((tid & 31) == 0) { gm.synw[c0 >> 5] = bx; gm.synw[p.nw + (c0 >> 5)] = bz; }
+                }
             }
-            group_sync<T>(g);
-            syn_bits = syndrome_bits<W, T>(p, gm, tid);
-            group_sync<T>(g);
+            // e_hat of iteration 1: hd0 on every qubit
+            const int nw1 = p.nw + 1;
+            for (int w = tid; w < 4 * nw1; w += T) {
+                const int wd = w % nw1, blk = w / nw1;
+                const int valid = p.ell - 32 * wd;
+                const uint32_t full = valid >= 32 ? 0xffffffffu : (valid > 0 ? (1u << valid) - 1u : 0u);
+                const uint32_t bit = (blk == kXL || blk == kXR) ? (hd0 & 1u) : (hd0 >> 1);
+                gm.bits[w] = bit ? full : 0u;
+            }
         } else {
-            syn_bits = 0;
-            int t = 0;
-            const uint8_t *s_in = p.syn_in + f * (long long)m;
-            for (int i = tid; i < m; i += T, ++t) syn_bits |= (s_in[i] != 0 ? 1u : 0u) << t;
+            if (p.sample) {
+                const uint64_t key1 = (uint64_t)(p.start + f);
+                const int nblk = (n + 3) >> 2;
+                for (int b = tid; b < nblk; b += T) {
+                    const U64x4 w = philox4x64_10((uint64_t)b + 1, p.seed, key1);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (4 * b + q < n) gm.ehat[4 * b + q] = pauli_from_word(w.v[q], p.kx, p.ky, p.kz);
+                }
+                group_sync<T>(g);
+                syn_bits = syndrome_bits_generic<T>(p, gm, tid);
+                group_sync<T>(g);
+            } else {
+                int t = 0;
+                const uint8_t *s_in = p.syn_in + f * (long long)m;
+                for (int i = tid; i < m; i += T, ++t) syn_bits |= (s_in[i] != 0 ? 1u : 0u) << t;
+            }
+            for (int j = tid; j < np_; j += T) gm.ehat[j] = hd0;
         }
-        for (int j = tid; j < np_; j += T) gm.ehat[j] = hd0;
         const uint32_t v0b = f2u(p.v0);
         for (int s = tid; s < msg_words; s += T) sts_u(gm.msg, 4u * s, v0b);
         group_sync<T>(g);
 
         int recorded = 0, success = 0, iters = p.l_max, n_gamma = 0, n_snap = 0;
         for (int ell = 1; ell <= p.l_max; ++ell) {
-            const uint32_t res = syn_bits ^ syndrome_bits<W, T>(p, gm, tid);
-            const int unsat = group_sum<T>(__popc(res), scratch, ell & 1, tid, g);
+            uint32_t res = 0;
+            int part;
+            if constexpr (W > 0) {
+                part = circ_syndrome<W, T>(p, gm, gm.synw, gm.resw, tid);
+            } else {
+                res = syn_bits ^ syndrome_bits_generic<T>(p, gm, tid);
+                part = __popc(res);
+            }
+            const int unsat = group_sum<T>(part, scratch, ell & 1, tid, g);
+            if constexpr (W > 0 && T == 32) __syncwarp();  // resw visible to the check phase
             if (p.tr_unsat && tid == 0) p.tr_unsat[f * p.l_max + n_gamma] = unsat;
             ++n_gamma;
             if (unsat == 0 && !recorded) {
@@ -515,12 +739,12 @@ __global__ void __launch_bounds__(512) decode_kernel(const KParams p)
                 iters = ell;
                 recorded = 1;
                 if (p.out_ehat)
-                    for (int j = tid; j < n; j += T) p.out_ehat[f * n + j] = (uint8_t)gm.ehat[j];
+                    for (int j = tid; j < n; j += T) p.out_ehat[f * n + j] = ehat_of<W>(p, gm, j);
             }
             if (p.early_stop && unsat == 0) break;
             if (ell == p.l_max) {
                 if (!recorded && p.out_ehat)
-                    for (int j = tid; j < n; j += T) p.out_ehat[f * n + j] = (uint8_t)gm.ehat[j];
+                    for (int j = tid; j < n; j += T) p.out_ehat[f * n + j] = ehat_of<W>(p, gm, j);
                 if (!capture) break;
             }
             float g0 = 1.0f, g1 = 1.0f;
@@ -550,7 +774,7 @@ __global__ void __launch_bounds__(512) decode_kernel(const KParams p)
         ++c_frames;
         c_fail += !success;
         c_iters += iters;
-        group_sync<T>(g);  // ehat/msg reuse by the next frame
+        group_sync<T>(g);  // group memory reuse by the next frame
     }
     if (p.counters && tid == 0 && c_frames) {
         atomicAdd((unsigned long long *)&p.counters[0], (unsigned long long)c_frames);

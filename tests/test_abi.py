@@ -50,7 +50,7 @@ def test_kernels_are_sm100a():
     assert "FFMA" in sass or len(sass) > 0
 
 
-@pytest.mark.parametrize("spec,kind", [(TOY, 2), (SMALL, 2), (GB126, 5), (GB254, 5), (GB1022, 5),
+@pytest.mark.parametrize("spec,kind", [(TOY, 0), (SMALL, 0), (GB126, 5), (GB254, 5), (GB1022, 5),
                                        ((127, (0, 15, 20), (0, 58, 59, 100)), 0)])
 def test_layout_compiler_host_only(oracle, spec, kind):
     import paper_2605_10433_b200 as P
