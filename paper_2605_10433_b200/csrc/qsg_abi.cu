@@ -162,7 +162,7 @@ int compile_layout(qsg_graph *g, int32_t n, int32_t m, const int64_t *cn_ptr, co
     // table-driven ones.
     int kind = 0;
     if (n % 2 == 0 && m == n && n / 2 >= 32 && dv_max % 2 == 0 && bicycle_w_supported(dv_max / 2) &&
-        (int64_t)dv_max * g->n_pad * 4 < (1 << 24)) {
+        (int64_t)dv_max * g->n_pad <= 65536) {
         const int32_t ell = n / 2, W = dv_max / 2;
         std::vector<int32_t> a, b;
         for (int64_t e = cn_ptr[0]; e < cn_ptr[1]; ++e)
@@ -211,7 +211,9 @@ int compile_layout(qsg_graph *g, int32_t n, int32_t m, const int64_t *cn_ptr, co
     // symbol in bits 30-31) and an info word at index dc_max (bicycle: 1 for
     // X checks, 0 for Z checks; generic: the degree).
     const int mp = g->m_pad, np_ = g->n_pad;
-    int rw = dc_max + 1;
+    // bicycle rows: 2W u16 slot indices (W words, made odd); generic rows:
+    // dc_max u32 entries + info word (made odd)
+    int rw = kind > 0 ? kind : dc_max + 1;
     if (rw % 2 == 0) ++rw;
     g->row_words = rw;
     std::vector<uint32_t> cn_tab((size_t)mp * rw, 0);
@@ -219,11 +221,13 @@ int compile_layout(qsg_graph *g, int32_t n, int32_t m, const int64_t *cn_ptr, co
     std::vector<int32_t> slot_edge((size_t)dv_max * np_, -1);
     for (int i = 0; i < m; ++i) {
         uint32_t *row = &cn_tab[(size_t)i * rw];
-        row[dc_max] = kind > 0 ? (edge_sym[cn_ptr[i]] == 1 ? 1u : 0u) : (uint32_t)(cn_ptr[i + 1] - cn_ptr[i]);
+        uint16_t *row16 = reinterpret_cast<uint16_t *>(row);
+        if (kind == 0) row[dc_max] = (uint32_t)(cn_ptr[i + 1] - cn_ptr[i]);
         for (int64_t e = cn_ptr[i]; e < cn_ptr[i + 1]; ++e) {
             const int k = (int)(e - cn_ptr[i]);
             const uint32_t slot = (uint32_t)pos_in_vn[e] * np_ + (uint32_t)edge_vn[e];
-            row[k] = slot * 4u | (kind > 0 ? 0u : (uint32_t)edge_sym[e] << 30);
+            if (kind > 0) row16[k] = (uint16_t)slot;
+            else row[k] = slot * 4u | (uint32_t)edge_sym[e] << 30;
             slot_edge[slot] = (int32_t)e;
         }
     }
@@ -253,7 +257,8 @@ int compile_layout(qsg_graph *g, int32_t n, int32_t m, const int64_t *cn_ptr, co
     g->tab_bytes = (uint32_t)((tab + 15) / 16 * 16);
     const int T = g->threads;
     size_t off = (size_t)dv_max * np_ * 4;             // messages
-    g->off_ehat = (uint32_t)off; off += (size_t)np_ * 4;
+    g->off_ehat = (uint32_t)off;
+    if (kind == 0) off += (size_t)np_ * 4;             // bicycle: aliases the messages
     g->off_bits = (uint32_t)off; off += (size_t)16 * (g->nw + 1);
     g->off_synw = (uint32_t)off; off += (size_t)8 * g->nw;
     g->off_resw = (uint32_t)off; off += (size_t)8 * g->nw;
@@ -298,7 +303,7 @@ int launch_cfg(qsg_graph *g, bool bp4, bool add, void *fn, qsg::LaunchCfg *out)
     int max_smem = 0;
     QSG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
     const int T = g->threads;
-    const int gmax = T == 32 ? 16 : 4;  // __launch_bounds__(512)
+    const int gmax = T == 32 ? 20 : 5;  // __launch_bounds__(640)
     qsg::LaunchCfg best;
     for (int G = 1; G <= gmax; ++G) {
         const size_t smem = g->tab_bytes + (size_t)G * g->group_bytes;

@@ -200,7 +200,7 @@ struct GroupMem {
     const uint8_t *vn_deg;   // generic only
     const int32_t *gbexp;    // bicycle: a exponents [0, 8), b exponents [8, 16)
     unsigned char *msg;      // fp32 messages, slot-major
-    uint32_t *ehat;          // generic: one Pauli code per qubit; bicycle: byte scratch
+    uint32_t *ehat;          // generic only: one Pauli code per qubit
     uint32_t *bits;          // bicycle: XL, ZL, XR, ZR circulant bitmaps, nw+1 words each
     uint32_t *synw;          // bicycle: observed syndrome words (X checks, then Z checks)
     uint32_t *resw;          // bicycle: residual syndrome words
@@ -304,10 +304,9 @@ __device__ __forceinline__ int circ_syndrome(const KParams &p, const GroupMem &g
 
 // Pack per-qubit Pauli codes (bytes in gm.ehat scratch) into the bitmaps.
 template <int T>
-__device__ __forceinline__ void bitmaps_from_bytes(const KParams &p, const GroupMem &gm, int tid)
+__device__ __forceinline__ void bitmaps_from_bytes(const KParams &p, const GroupMem &gm, const uint8_t *e, int tid)
 {
     const int l = p.ell;
-    const uint8_t *e = reinterpret_cast<const uint8_t *>(gm.ehat);
     const int nw1 = p.nw + 1;
     for (int c0 = tid & ~31; c0 < 32 * p.nw; c0 += T) {
         const int c = c0 + (tid & 31);
@@ -328,15 +327,21 @@ __device__ __forceinline__ void bitmaps_from_bytes(const KParams &p, const Group
 // the first-argmin rule (:325-333) without tracking the index.  Signs: the
 // extrinsic sign is (-1)^s_i * prod(sgn) * sgn_e (:314-316); messages are
 // never -0.0, so sgn_e is the IEEE sign bit and the product is an XOR.
+// Qubit->check messages are stored UNCLIPPED; the +-64 saturation of the
+// qubit update (decoder.py:358) is applied here where they are consumed:
+// every use is sign(v) or |clip(v)| = min(|v|, 64), and min1/min2 of the
+// clipped magnitudes are min(min1, 64), min(min2, 64) (clip is monotone),
+// with the |v_e| == min1 test unchanged whenever min1 < 64 and irrelevant
+// (min2 == min1 == 64) otherwise.
 template <int D, bool BP4>
-__device__ __forceinline__ void cn_update_fixed(const uint32_t *row, unsigned char *msg, uint32_t sneg, float gain)
+__device__ __forceinline__ void cn_update_fixed(const uint16_t *row, unsigned char *msg, uint32_t sneg, float gain)
 {
     uint32_t off[D];
     float v[D];
     uint32_t sx = sneg;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-        off[k] = row[k];
+        off[k] = 4u * row[k];  // bicycle rows hold u16 slot indices
         v[k] = lds_f(msg, off[k]);
         sx ^= f2u(v[k]);
     }
@@ -346,7 +351,7 @@ __device__ __forceinline__ void cn_update_fixed(const uint32_t *row, unsigned ch
         OptF o[D];
 #pragma unroll
         for (int k = 0; k < D; ++k) {
-            ph[k] = phi(fmaxf(fabsf(v[k]), 1e-12f));
+            ph[k] = phi(fmaxf(fminf(fabsf(v[k]), kClip), 1e-12f));
             o[k] = OptF{ph[k], true};
         }
         const float total = segsum_c<D>(o);
@@ -377,6 +382,8 @@ __device__ __forceinline__ void cn_update_fixed(const uint32_t *row, unsigned ch
             mn2 = fminf(mn2, fmaxf(mn1, a));
             mn1 = fminf(mn1, a);
         }
+        mn1 = fminf(mn1, kClip);
+        mn2 = fminf(mn2, kClip);
         const uint32_t m1 = f2u(fminf(gain * mn1, kClip)) ^ sgn;
         const uint32_t m2 = f2u(fminf(gain * mn2, kClip)) ^ sgn;
 #pragma unroll
@@ -408,8 +415,8 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, u
             auto one = [&](int h) {
                 const int wd = h * nw + (c >> 5);
                 const uint32_t sy = gm.synw[wd] >> bit, rs = gm.resw[wd] >> bit;
-                cn_update_fixed<2 * W, BP4>(gm.tab + (h * l + c) * p.row_words, msg, sy << 31,
-                                            (rs & 1u) ? g1 : g0);
+                cn_update_fixed<2 * W, BP4>(reinterpret_cast<const uint16_t *>(gm.tab + (h * l + c) * p.row_words),
+                                            msg, sy << 31, (rs & 1u) ? g1 : g0);
             };
             if constexpr (kUnrollPair<T, BP4>) {
                 one(0);
@@ -439,7 +446,7 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, u
             const uint32_t sgn = sx & 0x80000000u;
             if constexpr (BP4) {
                 float ph[kGenericMaxDeg];
-                for (int k = 0; k < d; ++k) ph[k] = phi(fmaxf(fabsf(v[k]), 1e-12f));
+                for (int k = 0; k < d; ++k) ph[k] = phi(fmaxf(fminf(fabsf(v[k]), kClip), 1e-12f));
                 const float total = segsum_rt(ph, d);
                 for (int k = 0; k < d; ++k) {
                     const float ext = fminf(fmaxf(total - ph[k], 1e-12f), 50.0f);
@@ -453,6 +460,8 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, u
                     mn2 = fminf(mn2, fmaxf(mn1, a));
                     mn1 = fminf(mn1, a);
                 }
+                mn1 = fminf(mn1, kClip);
+                mn2 = fminf(mn2, kClip);
                 const uint32_t m1 = f2u(fminf(gain * mn1, kClip)) ^ sgn;
                 const uint32_t m2 = f2u(fminf(gain * mn2, kClip)) ^ sgn;
                 for (int k = 0; k < d; ++k) {
@@ -492,13 +501,13 @@ __device__ __forceinline__ uint32_t vn_update_fixed(unsigned char *col, uint32_t
     const float bY = l0 + tY;
     if constexpr (ADD) {
 #pragma unroll
-        for (int s = 0; s < D; ++s) sts_u(col, s * rowb, f2u(clip64(l0 + (tY - c[s]))));
+        for (int s = 0; s < D; ++s) sts_u(col, s * rowb, f2u(l0 + (tY - c[s])));  // clipped by the consumer
     } else {
         // X-edge: self X, anti {Z, Y}; Z-edge: self Z, anti {X, Y}
         const float vX = logaddexp(0.0f, -bX) - logaddexp(-bZ, -bY);
         const float vZ = logaddexp(0.0f, -bZ) - logaddexp(-bX, -bY);
 #pragma unroll
-        for (int s = 0; s < D; ++s) sts_u(col, s * rowb, f2u(clip64((s < W ? vX : vZ) - c[s])));
+        for (int s = 0; s < D; ++s) sts_u(col, s * rowb, f2u((s < W ? vX : vZ) - c[s]));  // clipped by the consumer
     }
     return hard_decision(bX, bZ, bY);
 }
@@ -560,7 +569,7 @@ __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, i
             if constexpr (ADD) {
                 for (int s = 0; s < d; ++s) tmp[s] = c[s];
                 const float all = segsum_rt(tmp, d);
-                for (int s = 0; s < d; ++s) sts_u(col, s * rowb, f2u(clip64(l0 + (all - c[s]))));
+                for (int s = 0; s < d; ++s) sts_u(col, s * rowb, f2u(l0 + (all - c[s])));
             } else {
                 float V[4];
 #pragma unroll
@@ -568,19 +577,23 @@ __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, i
                     const int a1 = S == 1 ? 2 : 1, a2 = S == 3 ? 2 : 3;
                     V[S] = logaddexp(0.0f, -b[S]) - logaddexp(-b[a1], -b[a2]);
                 }
-                for (int s = 0; s < d; ++s) sts_u(col, s * rowb, f2u(clip64(V[sym[s]] - c[s])));
+                for (int s = 0; s < d; ++s) sts_u(col, s * rowb, f2u(V[sym[s]] - c[s]));
             }
         }
     }
 }
 
 template <int T>
-__device__ __forceinline__ void snapshot(const KParams &p, const unsigned char *msg, float *dst, int tid)
+__device__ __forceinline__ void snapshot(const KParams &p, const unsigned char *msg, float *dst, int tid,
+                                         bool clip)
 {
     const int total = p.dv_max * p.n_pad;
     for (int s = tid; s < total; s += T) {
         const int e = p.slot_edge[s];
-        if (e >= 0) dst[e] = lds_f(msg, 4u * s);
+        if (e >= 0) {
+            const float v = lds_f(msg, 4u * s);
+            dst[e] = clip ? clip64(v) : v;
+        }
     }
 }
 
@@ -601,7 +614,7 @@ __device__ __forceinline__ uint8_t ehat_of(const KParams &p, const GroupMem &gm,
 }
 
 template <int W, int T, bool BP4, bool ADD>
-__global__ void __launch_bounds__(512) decode_kernel(const KParams p)
+__global__ void __launch_bounds__(640) decode_kernel(const KParams p)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     // ---- per-CTA copy of the graph tables ----
@@ -661,7 +674,9 @@ __global__ void __launch_bounds__(512) decode_kernel(const KParams p)
         // ---- frame input: observed syndrome ----
         uint32_t syn_bits = 0;
         if constexpr (W > 0) {
-            uint8_t *eb = reinterpret_cast<uint8_t *>(gm.ehat);
+            // sampling scratch aliases the message area (initialised below,
+            // after the bitmaps are built)
+            uint8_t *eb = reinterpret_cast<uint8_t *>(gm.msg);
             if (p.sample) {
                 const uint64_t key1 = (uint64_t)(p.start + f);
                 const int nblk = (n + 3) >> 2;
@@ -673,7 +688,7 @@ __global__ void __launch_bounds__(512) decode_kernel(const KParams p)
                 }
                 for (int w = tid; w < 4 * (p.nw + 1); w += T) gm.bits[w] = 0u;
                 group_sync<T>(g);
-                bitmaps_from_bytes<T>(p, gm, tid);
+                bitmaps_from_bytes<T>(p, gm, eb, tid);
                 group_sync<T>(g);
                 circ_syndrome<W, T>(p, gm, nullptr, gm.synw, tid);
             } else {
@@ -758,11 +773,11 @@ __global__ void __launch_bounds__(512) decode_kernel(const KParams p)
             }
             cn_phase<W, T, BP4>(p, gm, syn_bits, res, g0, g1, tid);
             group_sync<T>(g);
-            if (capture && p.tr_cn) snapshot<T>(p, gm.msg, p.tr_cn + (f * p.l_max + n_snap) * p.E, tid);
+            if (capture && p.tr_cn) snapshot<T>(p, gm.msg, p.tr_cn + (f * p.l_max + n_snap) * p.E, tid, false);
             vn_phase<W, T, ADD>(p, gm, tid);
             group_sync<T>(g);
             if (capture) {
-                if (p.tr_vn) snapshot<T>(p, gm.msg, p.tr_vn + (f * p.l_max + n_snap) * p.E, tid);
+                if (p.tr_vn) snapshot<T>(p, gm.msg, p.tr_vn + (f * p.l_max + n_snap) * p.E, tid, true);
                 ++n_snap;
             }
         }
