@@ -182,8 +182,9 @@ def run_ours(args, rank, world, local_rank):
 
     import paper_2605_10433_b200 as P
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    dev_index = local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     g = P.gb_graph(P.GbSpec(*CODE))
     dg = P.device_graph(g, dev)
     decs = decoders(P)
@@ -211,7 +212,7 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize()
     step_ms, launch_ms = [], [[0.0, 0.0] for _ in points]
-    sampler = ClockSampler(local_rank)
+    sampler = ClockSampler(dev_index)
     with sampler:
         for _ in range(args.steps):
             flush_l2(l2)
@@ -350,8 +351,14 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dev_index = local_rank % torch.cuda.device_count()
+        torch.cuda.set_device(dev_index)
+        # QSG_BENCH_BACKEND=gloo exercises the multi-rank logic on one GPU
+        backend = os.environ.get("QSG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
     try:
         run_ours(args, rank, world, local_rank)
     finally:

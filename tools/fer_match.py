@@ -1,0 +1,92 @@
+"""FER match on shared frames: GPU outcomes vs the reference's float64
+arithmetic (the fp64 oracle, bit-exact with the reference for the min-sum
+family -- tests/test_oracle_pins.py).
+
+    python tools/fer_match.py gpu  --frames 32768      # on the B200 box
+    python tools/fer_match.py cpu  --frames 32768      # here: oracle fp64 + compare
+
+For every BASELINE configs[1] point the GPU decodes frames [0, F) and the
+per-frame fail flags are stored; the CPU side decodes the same frames with
+the fp64 restatement and reports both FERs, their 95% Wilson intervals, the
+paired flip counts, and whether each FER lies in the other's interval.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+PS = (0.02, 0.04, 0.06, 0.08, 0.10)
+NAMES = ("bp4", "sms0.5", "sms0.625", "sms0.75", "sms0.875", "sms1.0", "sagms")
+CODE = (127, (0, 15, 20, 28, 66), (0, 58, 59, 100, 121))
+
+
+def cfg_ns(name):
+    from types import SimpleNamespace as NS
+    gain = NS(alpha_min=0.30, alpha_max=0.50, eta_unsat=1.10) if name == "sagms" else None
+    alpha = float(name[3:]) if name.startswith("sms") else None
+    variant = "sms" if name.startswith("sms") else name
+    return NS(variant=variant, l_max=100, vn_mode="marginal", alpha=alpha, gain=gain)
+
+
+def gpu(frames, out):
+    import paper_2605_10433_b200 as P
+    g = P.gb_graph(P.GbSpec(*CODE))
+    res = {}
+    for p in PS:
+        for name in NAMES:
+            c = cfg_ns(name)
+            dcfg = P.DecoderConfig(c.variant, l_max=100, alpha=c.alpha,
+                                   gain=P.GainParams(0.30, 0.50, 1.10) if c.gain else None)
+            f, it = P.decode_frames(g, dcfg, p, p, 0, 0, frames)
+            res[f"{name}@{p}/fails"] = f
+            res[f"{name}@{p}/iters"] = it
+    np.savez_compressed(out, **res)
+
+
+def cpu(frames, gpu_npz, out):
+    from oracle import oracle as O
+    from paper_2605_10433_b200.harness import wilson_interval
+    g = O.Graph(O.gb_graph(*CODE))
+    d = np.load(gpu_npz)
+    rows = []
+    for p in PS:
+        for name in NAMES:
+            gf = d[f"{name}@{p}/fails"][:frames]
+            of, oit, _, _ = O.frames(g, cfg_ns(name), p, p, 0, 0, frames, precision=64)
+            o32, _, _, _ = O.frames(g, cfg_ns(name), p, p, 0, 0, frames, precision=32)
+            n = len(gf)
+            fg, fo = int(gf.sum()), int(of.sum())
+            lg, hg = wilson_interval(fg, n)
+            lo, ho = wilson_interval(fo, n)
+            rows.append({"point": f"{name}@{p}", "frames": n, "gpu_failures": fg, "ref64_failures": fo,
+                         "gpu_fer": fg / n, "ref64_fer": fo / n, "gpu_wilson95": [lg, hg],
+                         "ref64_wilson95": [lo, ho], "gpu_fer_in_ref_ci": lo <= fg / n <= ho,
+                         "frames_flipped": int((gf != of).sum()),
+                         "gpu_equals_fp32_oracle": bool(np.array_equal(gf, o32))})
+    summary = {"points": len(rows), "all_gpu_fer_in_ref_ci": all(r["gpu_fer_in_ref_ci"] for r in rows),
+               "all_gpu_equal_fp32_oracle": all(r["gpu_equals_fp32_oracle"] for r in rows),
+               "total_flipped_frames": sum(r["frames_flipped"] for r in rows),
+               "total_frames": sum(r["frames"] for r in rows)}
+    with open(out, "w") as fh:
+        json.dump({"summary": summary, "rows": rows}, fh, indent=1)
+    print(json.dumps(summary))
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("mode", choices=("gpu", "cpu"))
+    ap.add_argument("--frames", type=int, default=32768)
+    ap.add_argument("--gpu-npz", default=os.path.join(ROOT, "gpurun_out", "fer_gpu.npz"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "fer_match_r01.json"))
+    a = ap.parse_args()
+    if a.mode == "gpu":
+        gpu(a.frames, a.gpu_npz)
+    else:
+        cpu(a.frames, a.gpu_npz, a.out)
