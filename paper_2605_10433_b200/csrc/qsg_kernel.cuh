@@ -208,6 +208,24 @@ struct GroupMem {
 
 enum { kXL = 0, kZL = 1, kXR = 2, kZR = 3 };
 
+// ---- ALU-pipe relief -------------------------------------------------------
+// The bicycle kernels are bound by the half-rate ALU pipe (FMNMX / FSETP /
+// FSEL / LOP3 / PRMT); these helpers pin cheaper forms: a plain 16-bit shared
+// load (no PRMT unpacking of paired entries) and a single three-input LUT
+// for the sign merge (the compiler otherwise splits it in two).
+__device__ __forceinline__ uint32_t lds_u16(const uint16_t *p)
+{
+    uint32_t v;
+    asm("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+    return v;
+}
+__device__ __forceinline__ uint32_t sign_merge(uint32_t v, uint32_t mag)  // (v & 0x80000000) ^ mag
+{
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0x6a;" : "=r"(d) : "r"(v), "r"(0x80000000u), "r"(mag));
+    return d;
+}
+
 __device__ __forceinline__ float lds_f(const unsigned char *base, uint32_t off)
 {
     return *reinterpret_cast<const float *>(base + off);
@@ -341,7 +359,7 @@ __device__ __forceinline__ void cn_update_fixed(const uint16_t *row, unsigned ch
     uint32_t sx = sneg;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-        off[k] = 4u * row[k];  // bicycle rows hold u16 slot indices
+        off[k] = 4u * lds_u16(row + k);  // bicycle rows hold u16 slot indices
         v[k] = lds_f(msg, off[k]);
         sx ^= f2u(v[k]);
     }
@@ -389,7 +407,7 @@ __device__ __forceinline__ void cn_update_fixed(const uint16_t *row, unsigned ch
 #pragma unroll
         for (int k = 0; k < D; ++k) {
             const uint32_t mag = fabsf(v[k]) == mn1 ? m2 : m1;
-            sts_u(msg, off[k], (f2u(v[k]) & 0x80000000u) ^ mag);
+            sts_u(msg, off[k], sign_merge(f2u(v[k]), mag));
         }
     }
 }
