@@ -54,11 +54,32 @@ def decode_frames_device(graph, decoder_cfg, epsilon, epsilon0, seed, start, cou
     return fails, iters, ehat
 
 
+_PINNED: dict = {}
+
+
+def _pinned(nbytes: int) -> torch.Tensor:
+    """Grow-only pinned host staging buffer (one per thread and device)."""
+    import threading
+    key = (threading.get_ident(), torch.cuda.current_device())
+    buf = _PINNED.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
+        _PINNED[key] = buf
+    return buf
+
+
 def decode_frames(graph, decoder_cfg, epsilon, epsilon0, seed, start, count):
     """Drop-in for ``qsagms.harness._decode_frames``: returns numpy
-    (fails bool[count], iterations int64[count])."""
+    (fails bool[count], iterations int64[count]).  Results come back through
+    a pinned staging buffer with one stream synchronisation."""
     fails, iters, _ = decode_frames_device(graph, decoder_cfg, epsilon, epsilon0, seed, start, count)
-    return fails.cpu().numpy().astype(bool), iters.cpu().numpy()
+    stage = _pinned(9 * count)
+    it_h = stage[: 8 * count].view(torch.int64)
+    f_h = stage[8 * count: 9 * count]
+    it_h.copy_(iters, non_blocking=True)
+    f_h.copy_(fails, non_blocking=True)
+    torch.cuda.current_stream(iters.device).synchronize()
+    return f_h.numpy().astype(bool), it_h.numpy().copy()
 
 
 def install(harness_module) -> None:

@@ -161,3 +161,24 @@ def test_persistent_queue_partition_invariance(P):
     parts = [P.decode_frames(g, cfg, 0.08, 0.08, 9, s, c) for s, c in [(0, 1), (1, 999), (1000, 2000)]]
     assert np.array_equal(whole[0], np.concatenate([p[0] for p in parts]))
     assert np.array_equal(whole[1], np.concatenate([p[1] for p in parts]))
+
+
+# BASELINE configs 3-4 codes: every bicycle kernel instantiation (W = 3, 4, 5,
+# 6, 8; T = 32 and 128) against the oracle, bit for bit.
+CONFIG34_CODES = [(127, 3), (127, 4), (127, 6), (127, 8), (63, 5), (255, 5), (511, 5)]
+
+
+@pytest.mark.parametrize("ell,w", CONFIG34_CODES)
+@pytest.mark.parametrize("vn_mode", ["marginal", "additive"])
+def test_config34_codes_bit_exact(P, oracle, ell, w, vn_mode):
+    spec = P.random_gb_spec(ell, w, seed=0)
+    g = P.gb_graph(spec)
+    assert g.kind == w
+    B = 96 if ell >= 255 else 160
+    for variant, kw in CFGS:
+        cfg = _cfg(P, variant, kw, l_max=30, vn_mode=vn_mode)
+        fails, iters, ehat = P.decode_frames_device(g, cfg, 0.06, 0.06, 5, 100, B, want_ehat=True)
+        of, oi, oe, _ = oracle.frames(g, cfg, 0.06, 0.06, 5, 100, B, want_ehat=True)
+        assert np.array_equal(fails.cpu().numpy().astype(bool), of), (variant, vn_mode)
+        assert np.array_equal(iters.cpu().numpy(), oi), (variant, vn_mode)
+        assert np.array_equal(ehat.cpu().numpy(), oe), (variant, vn_mode)
