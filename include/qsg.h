@@ -11,6 +11,7 @@
  *                            _Kernel.syndromes_of decoder.py:303-309,
  *                            decode_batch decoder.py:374-485)
  *   qsg_decode_syndromes <- decoder.decode_batch        decoder.py:374-485
+ *   qsg_decode_syndromes_packed  same, bit-packed syndrome wire format
  *                           (+ collect_gamma / capture_messages traces used
  *                            by decoder.decode          decoder.py:488-559)
  *   qsg_sample_errors    <- channel.sample_error        channel.py:55-76
@@ -118,6 +119,14 @@ int qsg_decode_syndromes(const qsg_graph *g, const qsg_decoder_cfg *cfg, double 
                          const uint8_t *syndromes_dev, int64_t B, uint8_t *success_dev,
                          uint8_t *e_hat_dev, int64_t *iterations_dev, const qsg_trace *trace,
                          void *stream);
+
+/* decode_batch with bit-packed syndromes (32x less input traffic than one
+ * byte per check): syn_words_dev uint32[B * ceil(m/32)], bit i of frame b is
+ * (syn_words[b * ceil(m/32) + i/32] >> (i % 32)) & 1.  Outputs as in
+ * qsg_decode_syndromes (no traces). */
+int qsg_decode_syndromes_packed(const qsg_graph *g, const qsg_decoder_cfg *cfg, double l0,
+                                const uint32_t *syn_words_dev, int64_t B, uint8_t *success_dev,
+                                uint8_t *e_hat_dev, int64_t *iterations_dev, void *stream);
 
 /* _decode_frames: frames [start, start+count) sampled on device with
  * Philox4x64-10 keyed (seed, frame) exactly like sample_error, syndromes,

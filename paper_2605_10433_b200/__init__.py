@@ -42,7 +42,10 @@ from .decoder import (  # noqa: E402
     decode,
     decode_batch,
     decode_batch_device,
+    decode_batch_packed,
+    decode_batch_packed_device,
     effective_gain,
+    pack_syndromes,
     syndrome_ratio,
 )
 from . import dist  # noqa: E402,F401
@@ -69,7 +72,8 @@ __all__ = [
     "as_code_graph", "check_commute", "code_dimension", "csr_graph", "gb_dimension", "gb_graph",
     "load_qpc", "random_gb_spec", "save_qpc", "BatchDecodeResult", "DecodeResult",
     "DecoderConfig", "EdgeMessageState", "GainParams", "decode", "decode_batch",
-    "decode_batch_device", "effective_gain", "syndrome_ratio", "DeviceGraph", "device_graph",
+    "decode_batch_device", "decode_batch_packed", "decode_batch_packed_device", "pack_syndromes",
+    "effective_gain", "syndrome_ratio", "DeviceGraph", "device_graph",
     "FerPoint", "SweepConfig", "config_digest", "decode_frames", "decode_frames_device",
     "install", "run_point", "run_sweep", "wilson_interval", "build_gb_graph", "tanner_graph",
 ]

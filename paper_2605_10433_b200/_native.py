@@ -24,7 +24,8 @@ QSG_EUNSUPPORTED = -4
 #: Every symbol include/qsg.h declares (checked by tests/test_abi.py).
 EXPORTS = (
     "qsg_graph_create_gb", "qsg_graph_create_csr", "qsg_graph_destroy", "qsg_graph_info",
-    "qsg_graph_export", "qsg_decode_syndromes", "qsg_decode_frames", "qsg_sample_errors",
+    "qsg_graph_export", "qsg_decode_syndromes", "qsg_decode_syndromes_packed", "qsg_decode_frames",
+    "qsg_sample_errors",
     "qsg_syndromes_of", "qsg_last_error", "qsg_abi_version",
 )
 
@@ -78,6 +79,7 @@ def lib():
         L.qsg_graph_info.argtypes = [vp] + [vp] * 7
         L.qsg_graph_export.argtypes = [vp] * 7
         L.qsg_decode_syndromes.argtypes = [vp, vp, dbl, vp, i64, vp, vp, vp, vp, vp]
+        L.qsg_decode_syndromes_packed.argtypes = [vp, vp, dbl, vp, i64, vp, vp, vp, vp]
         L.qsg_decode_frames.argtypes = [vp, vp, dbl, dbl, u64, i64, i64, vp, vp, vp, vp, vp]
         L.qsg_sample_errors.argtypes = [i32, dbl, u64, i64, i64, vp, i32, vp]
         L.qsg_syndromes_of.argtypes = [vp, vp, i64, vp, vp]

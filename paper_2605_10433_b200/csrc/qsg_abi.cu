@@ -559,6 +559,32 @@ int qsg_decode_syndromes(const qsg_graph *gc, const qsg_decoder_cfg *cfg, double
     return launch_decode(g, cfg, p, (cudaStream_t)stream);
 }
 
+int qsg_decode_syndromes_packed(const qsg_graph *gc, const qsg_decoder_cfg *cfg, double l0,
+                                const uint32_t *syn_words_dev, int64_t B, uint8_t *success_dev,
+                                uint8_t *e_hat_dev, int64_t *iterations_dev, void *stream)
+{
+    qsg_graph *g = const_cast<qsg_graph *>(gc);
+    if (!g) return fail(QSG_EINVAL, "null graph");
+    if (g->device < 0) return fail(QSG_EINVAL, "graph was created host-only (device -1)");
+    int rc = validate_cfg(cfg);
+    if (rc) return rc;
+    if (B < 0) return fail(QSG_EINVAL, "negative batch size");
+    if (B > 0 && (!syn_words_dev || !success_dev || !iterations_dev)) return fail(QSG_EINVAL, "null buffer");
+    if (!std::isfinite(l0)) return fail(QSG_EINVAL, "prior llr must be finite");
+    DeviceGuard dg(g->device);
+    qsg::KParams p{};
+    fill_graph_params(g, p);
+    fill_cfg_params(cfg, l0, p);
+    p.sample = 0;
+    p.syn_words = syn_words_dev;
+    p.syn_wpf = (g->m + 31) / 32;
+    p.count = B;
+    p.out_flag = success_dev;
+    p.out_iters = iterations_dev;
+    p.out_ehat = e_hat_dev;
+    return launch_decode(g, cfg, p, (cudaStream_t)stream);
+}
+
 int qsg_decode_frames(const qsg_graph *gc, const qsg_decoder_cfg *cfg, double epsilon, double epsilon0,
                       uint64_t seed, int64_t start, int64_t count, uint8_t *fails_dev,
                       int64_t *iterations_dev, uint8_t *e_hat_dev, int64_t *counters_dev, void *stream)

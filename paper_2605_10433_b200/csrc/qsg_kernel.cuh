@@ -64,7 +64,9 @@ struct KParams {
     uint64_t seed;
     int64_t start;
     uint64_t kx, ky, kz;
-    const uint8_t *syn_in;
+    const uint8_t *syn_in;      // syndromes, one byte per check (decode_batch)
+    const uint32_t *syn_words;  // or bit-packed, syn_wpf words per frame
+    int32_t syn_wpf;
     int64_t count;
     // outputs
     uint8_t *out_flag;  // fails (sample) or success (syndromes)
@@ -709,6 +711,20 @@ __global__ void __launch_bounds__(640) decode_kernel(const KParams p)
                 bitmaps_from_bytes<T>(p, gm, eb, tid);
                 group_sync<T>(g);
                 circ_syndrome<W, T>(p, gm, nullptr, gm.synw, tid);
+            } else if (p.syn_words) {
+                // bit-packed rows: X checks are bits [0, l), Z checks [l, 2l)
+                const uint32_t *row = p.syn_words + f * (long long)p.syn_wpf;
+                const int l = p.ell;
+                for (int w = tid; w < 2 * p.nw; w += T) {
+                    const bool zc = w >= p.nw;
+                    const int ww = zc ? w - p.nw : w;
+                    const int start = (zc ? l : 0) + 32 * ww;
+                    const int q = start >> 5;
+                    const uint32_t hi = q + 1 < p.syn_wpf ? row[q + 1] : 0u;
+                    const uint32_t v = __funnelshift_r(row[q], hi, start & 31);
+                    const int valid = l - 32 * ww;
+                    gm.synw[w] = valid >= 32 ? v : v & ((1u << valid) - 1u);
+                }
             } else {
                 // observed syndrome rows: X checks c < l, Z checks l + c
                 const uint8_t *s_in = p.syn_in + f * (long long)m;
@@ -742,6 +758,10 @@ __global__ void __launch_bounds__(640) decode_kernel(const KParams p)
                 group_sync<T>(g);
                 syn_bits = syndrome_bits_generic<T>(p, gm, tid);
                 group_sync<T>(g);
+            } else if (p.syn_words) {
+                int t = 0;
+                const uint32_t *row = p.syn_words + f * (long long)p.syn_wpf;
+                for (int i = tid; i < m; i += T, ++t) syn_bits |= ((row[i >> 5] >> (i & 31)) & 1u) << t;
             } else {
                 int t = 0;
                 const uint8_t *s_in = p.syn_in + f * (long long)m;

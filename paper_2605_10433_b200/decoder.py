@@ -183,6 +183,44 @@ def decode_batch(graph, syndromes, prior: ChannelPrior, cfg, *, early_stop: bool
     return res
 
 
+def pack_syndromes(syndromes) -> np.ndarray:
+    """(B, m) syndrome bits -> (B, ceil(m/32)) uint32, bit i of row b at
+    word i // 32, bit i % 32 (the qsg_decode_syndromes_packed wire format)."""
+    syn = np.asarray(syndromes, dtype=np.uint8) != 0
+    B, m = syn.shape
+    pad = np.zeros((B, (m + 31) // 32 * 32), dtype=bool)
+    pad[:, :m] = syn
+    return np.packbits(pad, axis=1, bitorder="little").view("<u4").reshape(B, -1).astype(np.uint32)
+
+
+def decode_batch_packed_device(graph, syn_words: torch.Tensor, l0: float, cfg, *, e_hat=False):
+    """decode_batch from bit-packed device syndromes (uint32/int32 (B, ceil(m/32)))."""
+    import ctypes as C
+    dg = device_graph(graph, syn_words.device if syn_words.is_cuda else None)
+    dev = dg.device
+    if syn_words.dim() != 2 or syn_words.shape[1] != (dg.m + 31) // 32:
+        raise ValueError(f"packed syndromes must have shape (B, {(dg.m + 31) // 32})")
+    words = syn_words.to(device=dev).contiguous()
+    B = words.shape[0]
+    out = {"success": torch.empty(B, dtype=torch.uint8, device=dev),
+           "iterations": torch.empty(B, dtype=torch.int64, device=dev),
+           "e_hat": torch.empty((B, dg.n), dtype=torch.uint8, device=dev) if e_hat else None}
+    c = decoder_cfg_struct(cfg, True)
+    _native.check(_native.lib().qsg_decode_syndromes_packed(
+        dg.handle, C.byref(c), float(l0), ptr(words), B, ptr(out["success"]), ptr(out["e_hat"]),
+        ptr(out["iterations"]), stream_ptr(dev)))
+    return out
+
+
+def decode_batch_packed(graph, syn_words, prior: ChannelPrior, cfg) -> BatchDecodeResult:
+    """decode_batch for bit-packed syndromes (see pack_syndromes)."""
+    dg = device_graph(graph)
+    w = np.ascontiguousarray(syn_words, dtype=np.uint32).view(np.int32)
+    out = decode_batch_packed_device(dg, torch.from_numpy(w).to(dg.device), prior.llr, cfg, e_hat=True)
+    return BatchDecodeResult(success=out["success"].cpu().numpy().astype(bool),
+                             e_hat=out["e_hat"].cpu().numpy(), iterations=out["iterations"].cpu().numpy())
+
+
 def decode(H, graph, s, prior: ChannelPrior, cfg, *, early_stop: bool = True,
            capture_messages: bool = False, trace_sink=None) -> DecodeResult:
     """Single-syndrome decode with gamma trace and optional per-iteration

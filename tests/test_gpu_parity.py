@@ -182,3 +182,20 @@ def test_config34_codes_bit_exact(P, oracle, ell, w, vn_mode):
         assert np.array_equal(fails.cpu().numpy().astype(bool), of), (variant, vn_mode)
         assert np.array_equal(iters.cpu().numpy(), oi), (variant, vn_mode)
         assert np.array_equal(ehat.cpu().numpy(), oe), (variant, vn_mode)
+
+
+@pytest.mark.parametrize("spec", [SMALL, GB126, GB254, GB1022])
+def test_packed_syndromes_equal_byte_path(P, oracle, spec):
+    """Bit-packed syndrome wire format (qsg_decode_syndromes_packed) gives
+    the same outcomes as one byte per check."""
+    g = P.gb_graph(P.GbSpec(*spec))
+    e = oracle.sample_errors(g.n, 0.07, 4, 0, 200)
+    syn = oracle.syndromes_of(g, e)
+    words = P.pack_syndromes(syn)
+    assert words.shape == (200, (g.m + 31) // 32)
+    for variant, kw in CFGS:
+        cfg = _cfg(P, variant, kw, l_max=20)
+        a = P.decode_batch(g, syn, P.prior_llr(0.07), cfg)
+        b = P.decode_batch_packed(g, words, P.prior_llr(0.07), cfg)
+        assert np.array_equal(a.success, b.success) and np.array_equal(a.iterations, b.iterations)
+        assert np.array_equal(a.e_hat, b.e_hat)
