@@ -63,3 +63,20 @@ if __name__ == "__main__":
     p = lambda t: mp.log1p(t) / t if t != 0 else mp.mpf(1)
     for deg in (9, 10, 11):
         show(f"log1p P deg{deg}", *fit(p, 0, 1, deg, fixed=(1,)))
+
+
+def fit_phi():
+    """Division-free phi(x) = log1p(2/expm1(x)) pieces (BP4, qsg_math phi):
+      x >= ln2:  t = e^-x, phi = 2 atanh(t) = 2t + 2t u S(u), u = t^2 in [0, 1/4]
+      x <  ln2:  phi = ln2 - log(x) + v H(v),  v = x^2 in [0, ln2^2]
+                 (v H(v) = log((x/2) coth(x/2)), an even analytic function)"""
+    S = lambda u: (mp.atanh(mp.sqrt(u)) / mp.sqrt(u) - 1) / u if u != 0 else mp.mpf(1) / 3
+    Hf = lambda v: mp.log((mp.sqrt(v) / 2) * mp.coth(mp.sqrt(v) / 2)) / v if v != 0 else mp.mpf(1) / 12
+    for deg in (5, 6, 7):
+        show(f"phi S deg{deg}", *fit(S, 0, 0.25, deg))
+    for deg in (2, 3, 4):
+        show(f"phi H deg{deg}", *fit(Hf, 0, float(mp.log(2) ** 2), deg))
+
+
+if __name__ == "__main__" and "phi" in __import__("sys").argv:
+    fit_phi()
