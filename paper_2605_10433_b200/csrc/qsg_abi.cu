@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -303,7 +304,9 @@ int launch_cfg(qsg_graph *g, bool bp4, bool add, void *fn, qsg::LaunchCfg *out)
     int max_smem = 0;
     QSG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
     const int T = g->threads;
-    const int gmax = T == 32 ? 20 : 5;  // __launch_bounds__(640)
+    int gmax = T == 32 ? 20 : 5;  // __launch_bounds__(640)
+    int cap_sm = 1 << 30;         // QSG_MAX_FRAMES_PER_SM: tuning/diagnostics only
+    if (const char *env = std::getenv("QSG_MAX_FRAMES_PER_SM")) cap_sm = std::max(1, std::atoi(env));
     qsg::LaunchCfg best;
     for (int G = 1; G <= gmax; ++G) {
         const size_t smem = g->tab_bytes + (size_t)G * g->group_bytes;
@@ -311,6 +314,7 @@ int launch_cfg(qsg_graph *g, bool bp4, bool add, void *fn, qsg::LaunchCfg *out)
         QSG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int nb = 0;
         QSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, G * T, smem));
+        nb = std::min(nb, cap_sm / G);
         if (nb * G > best.ctas_per_sm * best.groups) {
             best.groups = G; best.ctas_per_sm = nb; best.smem = smem; best.ok = nb > 0;
         }
