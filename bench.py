@@ -32,10 +32,10 @@ sys.path.insert(0, ROOT)
 CODE = (127, (0, 15, 20, 28, 66), (0, 58, 59, 100, 121))
 PS = (0.02, 0.04, 0.06, 0.08, 0.10)
 SMS_ALPHAS = (0.5, 0.625, 0.75, 0.875, 1.0)
-FRAMES_PER_POINT = 1 << 20
+FRAMES_PER_POINT = int(os.environ.get("QSG_BENCH_FRAMES", 1 << 20))  # override: tests only
 L_MAX = 100
 SEED = 0
-CPU_SAMPLE_FRAMES = 1024  # per point, for the CPU legs
+CPU_SAMPLE_FRAMES = int(os.environ.get("QSG_BENCH_CPU_SAMPLE", 1024))  # per point, for the CPU legs
 METRIC = "decoded frames/s and CN-edge updates/s per GPU & 8×B200 (% roofline), FER match"
 # Algorithmic ops per CN-edge update: ALU + MUFU-class
 # ops of the reference algorithm, the numerator of roofline.achieved.

@@ -1,0 +1,45 @@
+"""The bench.py output contract (one JSON line with the driver's keys).
+The reference arm (CPU oracle port) runs here; the GPU arm in -m gpu."""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+             "scaling", "vs_baseline", "dtype", "data", "config", "e2e"}
+
+
+def _run(args, env_extra):
+    env = dict(os.environ, **env_extra)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True,
+                         text=True, env=env, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    return json.loads(lines[0])
+
+
+def test_reference_arm_contract():
+    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "3"], {"QSG_BENCH_CPU_SAMPLE": "16"})
+    assert BASE_KEYS <= set(d)
+    assert d["impl"] == "reference" and d["unit"] == "frames/s" and d["value"] > 0
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+@pytest.mark.gpu
+def test_gpu_arm_contract():
+    d = _run(["--steps", "1", "--warmup", "3"], {"QSG_BENCH_FRAMES": "16384", "QSG_BENCH_CPU_SAMPLE": "32"})
+    assert BASE_KEYS <= set(d) and "impl" not in d
+    assert d["gpu_launches"] == 35 and d["value"] > 0 and d["n_gpus"] == 1
+    r = d["roofline"]
+    assert r["bound"] == "issue" and 0 < r["frac"] <= 1.2 and r["peak"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert d["cpu_baseline"]["value"] > 0 and d["parity"].startswith("35/35")
+    assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}

@@ -8,10 +8,15 @@ codes = {"254": (127, (0, 15, 20, 28, 66), (0, 58, 59, 100, 121)),
          "1022": (511, (0, 5, 200, 397, 418), (0, 81, 284, 347, 418))}
 G = P.GainParams(0.3, 0.5, 1.1)
 cfgs = {"sagms": P.DecoderConfig("sagms", l_max=100, gain=G), "sms": P.DecoderConfig("sms", l_max=100, alpha=0.75),
-        "bp4": P.DecoderConfig("bp4", l_max=100), "sagms_add": P.DecoderConfig("sagms", l_max=100, gain=G, vn_mode="additive")}
+        "bp4": P.DecoderConfig("bp4", l_max=100), "sms": P.DecoderConfig("sms", l_max=100, alpha=0.75), "sagms_add": P.DecoderConfig("sagms", l_max=100, gain=G, vn_mode="additive")}
 frames = int(os.environ.get("FRAMES", 1 << 20))
 for code in sys.argv[1].split(","):
-    g = P.gb_graph(P.GbSpec(*codes[code]))
+    # "254", "1022", or "rgb<ell>w<w>" for random_gb_spec(ell, w, seed=0)
+    if code.startswith("rgb"):
+        ell, w = code[3:].split("w")
+        g = P.gb_graph(P.random_gb_spec(int(ell), int(w), seed=0))
+    else:
+        g = P.gb_graph(P.GbSpec(*codes[code]))
     dg = P.device_graph(g)
     for name in sys.argv[2].split(","):
         for p in [float(x) for x in sys.argv[3].split(",")]:
