@@ -86,7 +86,7 @@ def install(harness_module) -> None:
     """Route a reference harness module's FER loop through the GPU, e.g.
     ``install(qsagms.harness)``; run it with workers=1 (the GPU is the
     parallelism)."""
-    harness_module._decode_frames = decode_frames
+    harness_module._decode_frames = globals()["decode_frames"]
 
 
 # -- protocol (harness.py:44-158, 248-356) ----------------------------------------

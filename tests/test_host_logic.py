@@ -161,3 +161,35 @@ def test_marginal_init_formula():
     from paper_2605_10433_b200.decoder import marginal_init
     l0 = P.prior_llr(0.1).llr
     assert marginal_init(l0) == pytest.approx(math.log((0.9 + 0.1 / 3) / (2 * 0.1 / 3)), abs=1e-12)
+
+
+def test_install_routes_reference_harness(reference, monkeypatch, oracle):
+    """install(qsagms.harness) swaps the reference's FER unit
+    (harness.py:207-213 resolves _decode_frames by global name): the
+    reference's own run_point then calls ours.  Here ours is backed by the
+    CPU oracle (no GPU in this container); the result equals the
+    reference's own run_point."""
+    import qsagms.harness as RH
+    from qsagms.code import GbSpec, build_gb, tanner_graph
+    from qsagms.decoder import DecoderConfig
+
+    Hm = build_gb(GbSpec(3, (0, 1), (0, 2)))
+    g = tanner_graph(Hm)
+    cfg = RH.SweepConfig(code_id="toy", decoder=DecoderConfig("ms", l_max=1), epsilon_list=(0.5,), seed=2718,
+                         target_failures=50, max_frames=100_000)
+    want = RH.run_point(Hm, g, cfg, 0.5)
+    calls = []
+
+    def unit(graph, dcfg, eps, eps0, seed, start, count):
+        calls.append(count)
+        f, it, _, _ = oracle.frames(oracle.Graph(graph), dcfg, eps, eps0, seed, start, count, precision=64)
+        return f, it
+    monkeypatch.setattr(H, "decode_frames", unit)
+    original = RH._decode_frames
+    try:
+        P.install(RH)
+        assert RH._decode_frames is H.decode_frames is unit
+        got = RH.run_point(Hm, g, cfg, 0.5)
+    finally:
+        RH._decode_frames = original
+    assert calls and got == want and (got.frames, got.failures) == (56, 50)
