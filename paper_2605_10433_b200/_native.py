@@ -12,7 +12,9 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libqsg.so")
+# QSG_LIB overrides the library path (A/B timing of two builds in one process
+# tree; tools/ only).
+LIB_PATH = os.environ.get("QSG_LIB") or os.path.join(HERE, "libqsg.so")
 CSRC = os.path.join(HERE, "csrc")
 
 QSG_OK = 0

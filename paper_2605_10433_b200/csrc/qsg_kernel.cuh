@@ -228,6 +228,37 @@ __device__ __forceinline__ uint32_t sign_merge(uint32_t v, uint32_t mag)  // (v 
     return d;
 }
 
+// 32-bit shared-window addressing for the check phase: one LEA per edge
+// (slot * 4 + frame base) instead of an offset add plus a window add.
+// Volatile + clobber keep them ordered against the group barriers.
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ float lds_a(uint32_t a)
+{
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_a(uint32_t a, uint32_t v)
+{
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+// min(|a|, |b|) carrying sign(a) ^ sign(b): the check's sign product rides
+// along the min1 reduction for free (FMNMX.XORSIGN).
+__device__ __forceinline__ float min_xs(float a, float b)
+{
+    float d;
+    asm("min.xorsign.abs.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+// a ^ b kept opaque so the compiler cannot sink it below a select (which
+// would turn 2 XORs per check into one per edge).
+__device__ __forceinline__ uint32_t xor_pin(uint32_t a, uint32_t b)
+{
+    uint32_t d;
+    asm("xor.b32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+
 __device__ __forceinline__ float lds_f(const unsigned char *base, uint32_t off)
 {
     return *reinterpret_cast<const float *>(base + off);
@@ -354,19 +385,20 @@ __device__ __forceinline__ void bitmaps_from_bytes(const KParams &p, const Group
 // with the |v_e| == min1 test unchanged whenever min1 < 64 and irrelevant
 // (min2 == min1 == 64) otherwise.
 template <int D, bool BP4>
-__device__ __forceinline__ void cn_update_fixed(const uint16_t *row, unsigned char *msg, uint32_t sneg, float gain)
+__device__ __forceinline__ void cn_update_fixed(const uint16_t *row, uint32_t msg_s, uint32_t sneg, float gain)
 {
-    uint32_t off[D];
+    uint32_t ad[D];
     float v[D];
-    uint32_t sx = sneg;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-        off[k] = 4u * lds_u16(row + k);  // bicycle rows hold u16 slot indices
-        v[k] = lds_f(msg, off[k]);
-        sx ^= f2u(v[k]);
+        ad[k] = msg_s + 4u * lds_u16(row + k);  // bicycle rows hold u16 slot indices
+        v[k] = lds_a(ad[k]);
     }
-    const uint32_t sgn = sx & 0x80000000u;  // (-1)^s_i * prod sgn, as a sign bit
     if constexpr (BP4) {
+        uint32_t sx = sneg;
+#pragma unroll
+        for (int k = 0; k < D; ++k) sx ^= f2u(v[k]);
+        const uint32_t sgn = sx & 0x80000000u;  // (-1)^s_i * prod sgn, as a sign bit
         float ph[D];
         OptF o[D];
 #pragma unroll
@@ -379,37 +411,33 @@ __device__ __forceinline__ void cn_update_fixed(const uint16_t *row, unsigned ch
         for (int k = 0; k < D; ++k) {
             const float ext = fminf(fmaxf(total - ph[k], 1e-12f), 50.0f);
             const uint32_t mag = f2u(fminf(phi(ext), kClip)) ^ sgn;
-            sts_u(msg, off[k], (f2u(v[k]) & 0x80000000u) ^ mag);
+            sts_a(ad[k], (f2u(v[k]) & 0x80000000u) ^ mag);
         }
     } else {
         // smallest and second smallest of |v| (with multiplicity), two at a
-        // time: second' = min(second, max(min1, lo), hi)
+        // time: second' = min(second, max(min1, lo), hi).  min1 carries the
+        // XOR of all message signs in its sign bit.
         float mn1, mn2;
-        {
-            const float a = fabsf(v[0]), b = fabsf(v[1]);
-            mn1 = fminf(a, b);
-            mn2 = fmaxf(a, b);
-        }
+        mn1 = min_xs(v[0], v[1]);
+        mn2 = fmaxf(fabsf(v[0]), fabsf(v[1]));
 #pragma unroll
         for (int k = 2; k + 1 < D; k += 2) {
-            const float a = fabsf(v[k]), b = fabsf(v[k + 1]);
-            const float lo = fminf(a, b), hi = fmaxf(a, b);
-            mn2 = fminf(fminf(mn2, fmaxf(mn1, lo)), hi);
-            mn1 = fminf(mn1, lo);
+            const float lo = min_xs(v[k], v[k + 1]), hi = fmaxf(fabsf(v[k]), fabsf(v[k + 1]));
+            mn2 = fminf(fminf(mn2, fmaxf(fabsf(mn1), fabsf(lo))), hi);
+            mn1 = min_xs(mn1, lo);
         }
         if constexpr (D % 2) {
-            const float a = fabsf(v[D - 1]);
-            mn2 = fminf(mn2, fmaxf(mn1, a));
-            mn1 = fminf(mn1, a);
+            mn2 = fminf(mn2, fmaxf(fabsf(mn1), fabsf(v[D - 1])));
+            mn1 = min_xs(mn1, v[D - 1]);
         }
-        mn1 = fminf(mn1, kClip);
-        mn2 = fminf(mn2, kClip);
-        const uint32_t m1 = f2u(fminf(gain * mn1, kClip)) ^ sgn;
-        const uint32_t m2 = f2u(fminf(gain * mn2, kClip)) ^ sgn;
+        const uint32_t sgn = (f2u(mn1) ^ sneg) & 0x80000000u;  // (-1)^s_i * prod sgn
+        const float a1 = fminf(fabsf(mn1), kClip), a2 = fminf(mn2, kClip);
+        const uint32_t m1 = xor_pin(f2u(fminf(gain * a1, kClip)), sgn);
+        const uint32_t m2 = xor_pin(f2u(fminf(gain * a2, kClip)), sgn);
 #pragma unroll
         for (int k = 0; k < D; ++k) {
-            const uint32_t mag = fabsf(v[k]) == mn1 ? m2 : m1;
-            sts_u(msg, off[k], sign_merge(f2u(v[k]), mag));
+            const uint32_t mag = fabsf(v[k]) == a1 ? m2 : m1;
+            sts_a(ad[k], sign_merge(f2u(v[k]), mag));
         }
     }
 }
@@ -428,6 +456,7 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, u
     unsigned char *msg = gm.msg;
     if constexpr (W > 0) {
         const int l = p.ell, nw = p.nw;
+        const uint32_t msg_s = smem_addr(msg);
 #pragma unroll 1
         for (int c = tid; c < l; c += T) {
             const int bit = c & 31;
@@ -436,7 +465,7 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, u
                 const int wd = h * nw + (c >> 5);
                 const uint32_t sy = gm.synw[wd] >> bit, rs = gm.resw[wd] >> bit;
                 cn_update_fixed<2 * W, BP4>(reinterpret_cast<const uint16_t *>(gm.tab + (h * l + c) * p.row_words),
-                                            msg, sy << 31, (rs & 1u) ? g1 : g0);
+                                            msg_s, sy << 31, (rs & 1u) ? g1 : g0);
             };
             if constexpr (kUnrollPair<T, BP4>) {
                 one(0);
@@ -711,6 +740,7 @@ __global__ void __launch_bounds__(640) decode_kernel(const KParams p)
                 bitmaps_from_bytes<T>(p, gm, eb, tid);
                 group_sync<T>(g);
                 circ_syndrome<W, T>(p, gm, nullptr, gm.synw, tid);
+                group_sync<T>(g);  // every warp done reading the bitmaps before they are reset below
             } else if (p.syn_words) {
                 // bit-packed rows: X checks are bits [0, l), Z checks [l, 2l)
                 const uint32_t *row = p.syn_words + f * (long long)p.syn_wpf;

@@ -199,3 +199,17 @@ def test_packed_syndromes_equal_byte_path(P, oracle, spec):
         b = P.decode_batch_packed(g, words, P.prior_llr(0.07), cfg)
         assert np.array_equal(a.success, b.success) and np.array_equal(a.iterations, b.iterations)
         assert np.array_equal(a.e_hat, b.e_hat)
+
+
+@pytest.mark.parametrize("spec,variant", [(GB1022, "sms"), (GB254, "sagms")])
+def test_full_occupancy_runs_are_deterministic(P, spec, variant):
+    """2^20 sampled frames at full occupancy, twice: per-frame outcomes are
+    identical (catches intra-frame races between warps of a group, which
+    only show up when the SM is saturated -- a missing barrier between the
+    sampled-syndrome pass and the bitmap reset once flipped ~3 frames per
+    million on the 128-thread kernels)."""
+    g = P.gb_graph(P.GbSpec(*spec))
+    cfg = _cfg(P, variant, dict(CFGS)[variant], l_max=100)
+    runs = [P.decode_frames_device(g, cfg, 0.08, 0.08, 0, 0, 1 << 20) for _ in range(3)]
+    for f, it, _ in runs[1:]:
+        assert torch.equal(f, runs[0][0]) and torch.equal(it, runs[0][1])
