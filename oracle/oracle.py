@@ -253,7 +253,7 @@ def prior_llr(epsilon0):
     return math.log(3.0 * (1.0 - epsilon0) / epsilon0)
 
 
-MATH_FUNCS = {"exp_neg": 0, "log1p_01": 1, "log1p": 2, "expm1": 3, "logaddexp": 4, "phi": 5}
+MATH_FUNCS = {"exp_neg": 0, "log1p_01": 1, "log1p": 2, "expm1": 3, "logaddexp": 4, "phi": 5, "vnF": 6}
 
 
 def math32(name, x, y=None):

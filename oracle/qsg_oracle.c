@@ -144,6 +144,7 @@ void qsgo_math32_batch(int32_t which, const float *x, const float *y, float *out
         case 3: out[i] = qo_expm1(x[i]); break;
         case 4: out[i] = qo_logaddexp(x[i], y[i]); break;
         case 5: out[i] = qo_phi(x[i]); break;
+        case 6: out[i] = qo_vnF(x[i], qo_vn_kapc(y[i])); break;
         default: out[i] = NAN;
         }
     }

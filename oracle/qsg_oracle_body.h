@@ -76,6 +76,9 @@ static void QF(_decode_one)(const qsgo_graph *g, const qsgo_cfg *cfg, REAL l0, R
     const int n = g->n, m = g->m;
     const REAL CLIP = (REAL)64.0;
     const int capture = (tr_vn != NULL || tr_cn != NULL);
+#if VN_FACTORED
+    const float kapc = qo_vn_kapc((float)l0);
+#endif
     for (int64_t e = 0; e < E; ++e) { s->vmsg[e] = v0; s->cmsg[e] = (REAL)0.0; }
     int recorded = 0, success = 0, n_gamma = 0, n_snap = 0;
     int64_t iters = cfg->l_max;
@@ -189,9 +192,20 @@ static void QF(_decode_one)(const qsgo_graph *g, const qsgo_cfg *cfg, REAL l0, R
                  * LAE(0, -(l0 + tot_S)) - LAE(-(l0 + tot_a1), -(l0 + tot_a2))
                  * once per qubit and symbol (a1/a2 as selected at :355-356). */
                 REAL V[4];
-                for (int S = 1; S <= 3; ++S) {
-                    int a1 = S == 1 ? 2 : 1, a2 = S == 3 ? 2 : 3;
-                    V[S] = LAE((REAL)0.0, -(l0 + tot[S])) - LAE(-(l0 + tot[a1]), -(l0 + tot[a2]));
+                int has_y = 0;
+                for (int64_t q = 0; q < d; ++q) has_y |= g->edge_sym[g->vn_order[p0 + q]] == 3;
+                if (!has_y) {
+                    /* no Y-type edge: tot[1] = S_Z, tot[2] = S_X and
+                     * V[X] = (l0 + S_X) + F(S_Z), V[Z] = (l0 + S_Z) + F(S_X)
+                     * (qo_vnF, the kernels' vn_F) */
+                    V[1] = (l0 + tot[2]) + qo_vnF(tot[1], kapc);
+                    V[2] = (l0 + tot[1]) + qo_vnF(tot[2], kapc);
+                    V[3] = (REAL)0.0;
+                } else {
+                    for (int S = 1; S <= 3; ++S) {
+                        int a1 = S == 1 ? 2 : 1, a2 = S == 3 ? 2 : 3;
+                        V[S] = LAE((REAL)0.0, -(l0 + tot[S])) - LAE(-(l0 + tot[a1]), -(l0 + tot[a2]));
+                    }
                 }
                 for (int64_t q = 0; q < d; ++q) {
                     uint8_t sym = g->edge_sym[g->vn_order[p0 + q]];

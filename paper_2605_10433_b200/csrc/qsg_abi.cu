@@ -368,6 +368,8 @@ void fill_cfg_params(const qsg_decoder_cfg *c, double l0, qsg::KParams &p)
     p.l_max = c->l_max;
     p.early_stop = c->early_stop ? 1 : 0;
     p.l0 = (float)l0;
+    // vn_F constant from the fp32 prior, in double (the oracle's qo_vn_kapc)
+    p.kapc = (float)std::exp(-(double)p.l0);
     // decoder.py:405-406 (marginal init :255-261), double then one rounding
     double v0 = c->vn_mode == QSG_VN_MARGINAL ? std::log1p(std::exp(-l0)) + l0 - 0.6931471805599453 : l0;
     v0 = std::min(64.0, std::max(-64.0, v0));

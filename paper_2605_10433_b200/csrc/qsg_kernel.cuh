@@ -58,6 +58,7 @@ struct KParams {
     int32_t gain_mode;  // 0: none (bp4/ms), 1: constant alpha (sms), 2: sagms
     int32_t l_max, early_stop;
     float l0, v0, alpha;
+    float kapc;  // e^-l0 (vn_F)
     double amin, amax, eta;
     // input
     int32_t sample;  // 1: sample frames on device; 0: read syndromes
@@ -399,20 +400,35 @@ __device__ __forceinline__ void cn_update_fixed(const uint16_t *row, uint32_t ms
 #pragma unroll
         for (int k = 0; k < D; ++k) sx ^= f2u(v[k]);
         const uint32_t sgn = sx & 0x80000000u;  // (-1)^s_i * prod sgn, as a sign bit
-        float ph[D];
+        // The forward phi(|v|) is evaluated on the x >= ln2 side only when
+        // every active lane of the warp has all its arguments there (a
+        // warp-uniform branch, the common case); otherwise, and always for
+        // the extrinsic phi (whose arguments straddle ln 2 in most warps,
+        // measured), both sides with a select.
+        const unsigned act = __activemask();
+        float x[D], ph[D];
+        float xmin = kClip;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            x[k] = fmaxf(fminf(fabsf(v[k]), kClip), 1e-12f);
+            xmin = fminf(xmin, x[k]);
+        }
+        if (__all_sync(act, xmin >= kLn2f)) {
+#pragma unroll
+            for (int k = 0; k < D; ++k) ph[k] = phi_hi(x[k]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < D; ++k) ph[k] = phi(x[k]);
+        }
         OptF o[D];
 #pragma unroll
-        for (int k = 0; k < D; ++k) {
-            ph[k] = phi(fmaxf(fminf(fabsf(v[k]), kClip), 1e-12f));
-            o[k] = OptF{ph[k], true};
-        }
+        for (int k = 0; k < D; ++k) o[k] = OptF{ph[k], true};
         const float total = segsum_c<D>(o);
+        float r[D];
 #pragma unroll
-        for (int k = 0; k < D; ++k) {
-            const float ext = fminf(fmaxf(total - ph[k], 1e-12f), 50.0f);
-            const uint32_t mag = f2u(fminf(phi(ext), kClip)) ^ sgn;
-            sts_a(ad[k], (f2u(v[k]) & 0x80000000u) ^ mag);
-        }
+        for (int k = 0; k < D; ++k) r[k] = phi(fminf(fmaxf(total - ph[k], 1e-12f), 50.0f));
+#pragma unroll
+        for (int k = 0; k < D; ++k) sts_a(ad[k], (f2u(v[k]) & 0x80000000u) ^ f2u(fminf(r[k], kClip)) ^ sgn);
     } else {
         // smallest and second smallest of |v| (with multiplicity), two at a
         // time: second' = min(second, max(min1, lo), hi).  min1 carries the
@@ -531,7 +547,7 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, u
 // oracle's fp32 path uses the same factorisation, its fp64 path the
 // reference's literal per-edge form).  Returns the hard decision.
 template <int W, bool ADD>
-__device__ __forceinline__ uint32_t vn_update_fixed(unsigned char *col, uint32_t rowb, float l0)
+__device__ __forceinline__ uint32_t vn_update_fixed(unsigned char *col, uint32_t rowb, float l0, float kapc)
 {
     constexpr int D = 2 * W;
     float c[D];
@@ -544,28 +560,30 @@ __device__ __forceinline__ uint32_t vn_update_fixed(unsigned char *col, uint32_t
         oz[s] = OptF{c[s], s < W};
         oa[s] = OptF{c[s], true};
     }
-    const float bX = l0 + segsum_c<D>(ox);
-    const float bZ = l0 + segsum_c<D>(oz);
+    const float sZ = segsum_c<D>(ox), sX = segsum_c<D>(oz);  // tot_X, tot_Z
+    const float bX = l0 + sZ;
+    const float bZ = l0 + sX;
     const float tY = segsum_c<D>(oa);
     const float bY = l0 + tY;
     if constexpr (ADD) {
 #pragma unroll
         for (int s = 0; s < D; ++s) sts_u(col, s * rowb, f2u(l0 + (tY - c[s])));  // clipped by the consumer
     } else {
-        // X-edge: self X, anti {Z, Y}; Z-edge: self Z, anti {X, Y}
-        const float vX = logaddexp(0.0f, -bX) - logaddexp(-bZ, -bY);
-        const float vZ = logaddexp(0.0f, -bZ) - logaddexp(-bX, -bY);
+        // X-edge: self X, anti {Z, Y}; Z-edge: self Z, anti {X, Y}; no Y
+        // edges, so V[X] = b_Z + F(S_Z), V[Z] = b_X + F(S_X) (vn_F)
+        const float vX = bZ + vn_F(sZ, kapc);
+        const float vZ = bX + vn_F(sX, kapc);
 #pragma unroll
         for (int s = 0; s < D; ++s) sts_u(col, s * rowb, f2u((s < W ? vX : vZ) - c[s]));  // clipped by the consumer
     }
     return hard_decision(bX, bZ, bY);
 }
 
-template <int W, int T, bool ADD>
+template <int W, int T, bool BP4, bool ADD>
 __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, int tid)
 {
     const uint32_t rowb = (uint32_t)p.n_pad * 4;
-    const float l0 = p.l0;
+    const float l0 = p.l0, kapc = p.kapc;
     unsigned char *msg = gm.msg;
     if constexpr (W > 0) {
         // thread owns qubits c and l + c; the warp ballots their hard
@@ -576,12 +594,12 @@ __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, i
             const int c = c0 + (tid & 31);
             uint32_t e2[2] = {0u, 0u};
             if (c < l) {
-                if constexpr (kUnrollPair<T, false>) {
-                    e2[0] = vn_update_fixed<W, ADD>(msg + 4 * c, rowb, l0);
-                    e2[1] = vn_update_fixed<W, ADD>(msg + 4 * (l + c), rowb, l0);
+                if constexpr (kUnrollPair<T, BP4>) {
+                    e2[0] = vn_update_fixed<W, ADD>(msg + 4 * c, rowb, l0, kapc);
+                    e2[1] = vn_update_fixed<W, ADD>(msg + 4 * (l + c), rowb, l0, kapc);
                 } else {
 #pragma unroll 1
-                    for (int h = 0; h < 2; ++h) e2[h] = vn_update_fixed<W, ADD>(msg + 4 * (h * l + c), rowb, l0);
+                    for (int h = 0; h < 2; ++h) e2[h] = vn_update_fixed<W, ADD>(msg + 4 * (h * l + c), rowb, l0, kapc);
                 }
             }
             const uint32_t eL = e2[0], eR = e2[1];
@@ -604,7 +622,7 @@ __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, i
                 c[s] = lds_f(col, s * rowb);
                 sym[s] = gm.vn_sym[s * p.n_pad + j];
             }
-            float b[4];
+            float b[4], tot[4];
 #pragma unroll
             for (int e = 1; e <= 3; ++e) {
                 for (int s = 0; s < d; ++s) {
@@ -612,8 +630,10 @@ __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, i
                     const uint32_t a = e == 1 ? sz : (e == 2 ? sx : (sx ^ sz));
                     tmp[s] = a ? c[s] : 0.0f;
                 }
-                b[e] = l0 + segsum_rt(tmp, d);
+                tot[e] = segsum_rt(tmp, d);
+                b[e] = l0 + tot[e];
             }
+            const float sumz = tot[1], sumx = tot[2];
             gm.ehat[j] = hard_decision(b[1], b[2], b[3]);
             if constexpr (ADD) {
                 for (int s = 0; s < d; ++s) tmp[s] = c[s];
@@ -621,10 +641,18 @@ __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, i
                 for (int s = 0; s < d; ++s) sts_u(col, s * rowb, f2u(l0 + (all - c[s])));
             } else {
                 float V[4];
+                uint32_t any_y = 0;
+                for (int s = 0; s < d; ++s) any_y |= sym[s] == 3;
+                if (!any_y) {  // b[1] - l0 = S_Z, b[2] - l0 = S_X exactly as summed
+                    V[1] = b[2] + vn_F(sumz, kapc);
+                    V[2] = b[1] + vn_F(sumx, kapc);
+                    V[3] = 0.0f;
+                } else {
 #pragma unroll
-                for (int S = 1; S <= 3; ++S) {
-                    const int a1 = S == 1 ? 2 : 1, a2 = S == 3 ? 2 : 3;
-                    V[S] = logaddexp(0.0f, -b[S]) - logaddexp(-b[a1], -b[a2]);
+                    for (int S = 1; S <= 3; ++S) {
+                        const int a1 = S == 1 ? 2 : 1, a2 = S == 3 ? 2 : 3;
+                        V[S] = logaddexp(0.0f, -b[S]) - logaddexp(-b[a1], -b[a2]);
+                    }
                 }
                 for (int s = 0; s < d; ++s) sts_u(col, s * rowb, f2u(V[sym[s]] - c[s]));
             }
@@ -842,7 +870,7 @@ __global__ void __launch_bounds__(640) decode_kernel(const KParams p)
             cn_phase<W, T, BP4>(p, gm, syn_bits, res, g0, g1, tid);
             group_sync<T>(g);
             if (capture && p.tr_cn) snapshot<T>(p, gm.msg, p.tr_cn + (f * p.l_max + n_snap) * p.E, tid, false);
-            vn_phase<W, T, ADD>(p, gm, tid);
+            vn_phase<W, T, BP4, ADD>(p, gm, tid);
             group_sync<T>(g);
             if (capture) {
                 if (p.tr_vn) snapshot<T>(p, gm.msg, p.tr_vn + (f * p.l_max + n_snap) * p.E, tid, true);

@@ -1,6 +1,7 @@
 // Test harness: the PRODUCT's fp32 recipes (qsg_math.cuh) compiled for the
 // host, so tests/test_oracle_math.py can check they equal the oracle's
 // independent copy bit-for-bit.
+#include <math.h>
 #include <stdint.h>
 #include "../../paper_2605_10433_b200/csrc/qsg_math.cuh"
 
@@ -14,6 +15,7 @@ extern "C" void qsg_math_host_batch(int32_t which, const float *x, const float *
         case 3: out[i] = qsg::expm1_pos(x[i]); break;
         case 4: out[i] = qsg::logaddexp(x[i], y[i]); break;
         case 5: out[i] = qsg::phi(x[i]); break;
+        case 6: out[i] = qsg::vn_F(x[i], (float)exp(-(double)y[i])); break;  // kapc as the ABI computes it
         default: out[i] = 0.0f;
         }
     }

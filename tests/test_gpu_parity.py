@@ -78,7 +78,9 @@ def test_config1_golden(P, oracle):
     assert np.nonzero(fails)[0].tolist() == [356, 813, 951, 3063, 3175, 4838, 5302, 5579, 6030,
                                              6972, 7982, 8244]
     assert int(iters.sum()) == 45_097
-    assert digest(ehat) == "851c8b33a191d199"
+    # the reference's e_hat digest is 851c8b33a191d199; the fp32 recipe's
+    # differs only in failing frame 5579 (attributed in test_oracle_pins.py)
+    assert digest(ehat) == "1e681528efa09e6e"
     of, oi, oe, _ = oracle.frames(g, cfg, 0.05, 0.05, 0, 0, 10_000, want_ehat=True)
     assert np.array_equal(fails.astype(bool), of) and np.array_equal(iters, oi) and np.array_equal(ehat, oe)
     # counters path

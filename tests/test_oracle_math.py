@@ -19,7 +19,7 @@ import numpy as np
 import pytest
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-FUNCS = {"exp_neg": 0, "log1p_01": 1, "log1p": 2, "expm1": 3, "logaddexp": 4, "phi": 5}
+FUNCS = {"exp_neg": 0, "log1p_01": 1, "log1p": 2, "expm1": 3, "logaddexp": 4, "phi": 5, "vnF": 6}
 
 
 @pytest.fixture(scope="module")
@@ -50,6 +50,12 @@ def _args(name, rng, n=200_000):
         return np.concatenate([rng.uniform(1e-12, 64, n), 10.0 ** rng.uniform(-12, 0, n // 2)]), None
     if name == "phi":
         return np.concatenate([rng.uniform(1e-12, 64, n), 10.0 ** rng.uniform(-12, 1.5, n // 2)]), None
+    if name == "vnF":  # (y, l0): message sums over the decoder's range, priors of p in [1e-4, 0.7]
+        p = 10.0 ** rng.uniform(-4, np.log10(0.7), n)
+        l0 = np.log(3.0 * (1.0 - p) / p)
+        y = np.concatenate([rng.uniform(-700, 700, n // 2), rng.standard_normal(n - n // 2) * 10.0 ** rng.integers(-6, 2, n - n // 2)])
+        y[:4] = [0.0, -0.0, 87.5, -87.5]
+        return y, l0
     x = rng.uniform(-70, 70, n)
     y = x + rng.standard_normal(n) * 10.0 ** rng.integers(-8, 3, n)
     y[:1000] = x[:1000]  # exact ties exercise the x == y branch
@@ -111,6 +117,24 @@ def test_recipe_accuracy(oracle, name, max_ulp):
     err = _ulp_err(got, ref)
     mask = np.abs(ref) > 1e-30
     assert err[mask].max() <= max_ulp, (name, err[mask].max())
+
+
+def test_vn_factor_accuracy(oracle):
+    """F(y) = log((1 + e^-l0 e^-y) / (1 + e^-y)), the qubit-update factor
+    (V[X] = b_Z + F(S_Z)): error <= 2.5e-7 + 1 ulp(F) against the literal
+    two-logaddexp form evaluated in long double, over |y| <= 700 and priors
+    of p in [1e-4, 0.7] (|F| <= |l0| <= 10.3)."""
+    L = _libm_long_double()
+    rng = np.random.default_rng(7)
+    y, l0 = _args("vnF", rng, 20_000)
+    y32, l032 = y.astype(np.float32), l0.astype(np.float32)
+    got = oracle.math32("vnF", y32, l032).astype(np.float64)
+
+    def lae0(z):  # logaddexp(0, z)
+        return max(z, 0.0) + float(L.log1pl(L.expl(-abs(z))))
+    ref = np.array([lae0(-(float(a) + float(b))) - lae0(-float(b)) for a, b in zip(l032, y32)])
+    err = np.abs(got - ref) / (2.5e-7 + np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64))
+    assert err.max() <= 1.0, (err.max(), y32[err.argmax()], l032[err.argmax()])
 
 
 def test_exact_identities(oracle, host_math):

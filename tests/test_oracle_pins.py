@@ -96,6 +96,9 @@ def test_numpy_reduceat_tree(oracle, dtype, d):
             assert dtype(seg[0] + pairwise(seg[1:])) == got[b, s]
 
 
+EHAT32_CONFIG1 = "1e681528efa09e6e"  # fp32 recipe (GPU == oracle32), see below
+
+
 @pytest.mark.parametrize("precision", [32, 64])
 def test_config1_golden(oracle, precision):
     gold = json.load(open(os.path.join(GOLD, "golden_config1.json")))
@@ -106,8 +109,21 @@ def test_config1_golden(oracle, precision):
     r = oracle.decode(g, syn, oracle.prior_llr(0.05), cfg("sagms", 100), precision=precision)
     assert np.nonzero(~r.success)[0].tolist() == gold["fail_frames"]
     assert int(r.iterations.sum()) == gold["sum_iterations"]
-    assert digest(r.e_hat) == gold["ehat_sha16"]
     assert np.bincount(r.iterations, minlength=101)[:16].tolist() == gold["iteration_hist_0_15"]
+    if precision == 64:
+        assert digest(r.e_hat) == gold["ehat_sha16"]
+    else:
+        # fp32 (== the GPU): same outcomes and iteration counts on all 10^4
+        # frames; the final e_hat of one FAILING frame (kept from iteration
+        # 100) differs -- its trajectory splits from float64 at iteration 96
+        # after rounding growth (attributed below).
+        assert digest(r.e_hat) == EHAT32_CONFIG1
+        r64 = oracle.decode(g, syn, oracle.prior_llr(0.05), cfg("sagms", 100), precision=64)
+        differ = np.nonzero((r.e_hat != r64.e_hat).any(axis=1))[0].tolist()
+        assert differ == [5579] and not r.success[5579]
+        from oracle.attribution import attribute
+        a = attribute(g, syn[5579], oracle.prior_llr(0.05), cfg("sagms", 100), frame=5579)
+        assert a.attributed and a.kind == "rounding-growth", a
 
 
 @pytest.fixture(scope="module")
