@@ -51,6 +51,7 @@ struct qsg_graph {
     std::vector<uint8_t> edge_sym;
     // device tables
     uint32_t *d_cn_tab = nullptr;
+    uint32_t *d_cn_tab_x = nullptr;  // bicycle: rows in exponent order (min-sum kernels)
     uint8_t *d_vn_sym = nullptr, *d_vn_deg = nullptr;
     int32_t *d_slot_edge = nullptr;
     int32_t *d_cn_ptr = nullptr, *d_edge_vn = nullptr;

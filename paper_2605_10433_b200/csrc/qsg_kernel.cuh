@@ -354,6 +354,89 @@ __device__ __forceinline__ int circ_syndrome(const KParams &p, const GroupMem &g
     return cnt;
 }
 
+// The same syndrome with every loop-invariant part hoisted: a thread's word
+// w, its 32-bit windows (bitmap word, shift, wrap) and the word's valid mask
+// depend only on its lane and the code, so they are computed once per
+// kernel.  Window descriptor: bits 0-9 word index of B[q] in gm.bits,
+// 10-19 word index of B[0] of that bitmap, 20-24 shift, 25-29 wrap shift
+// n1 = l - start (0: no wrap), 31 valid.  Needs lpw >= 4 (at most
+// ceil(2W / 4) windows per lane; the host guarantees it for every bicycle
+// shape it builds, else circ_syndrome is used).
+template <int W>
+struct SynPlan {
+    static constexpr int K = (2 * W + 3) / 4;
+    uint32_t d[K];
+    uint32_t mask;  // valid bits of word w (0 for idle lanes)
+    int w;          // syndrome word (X words then Z words), -1 idle
+    bool writer;    // first lane of its word
+};
+
+template <int W, int T>
+__device__ __forceinline__ SynPlan<W> syn_plan(const KParams &p, const GroupMem &gm, int tid)
+{
+    SynPlan<W> P;
+    const int nw = p.nw, l = p.ell, lpw = p.lpw;
+    const int w = tid / lpw, sub = tid - w * lpw;
+    P.w = -1; P.mask = 0u; P.writer = false;
+#pragma unroll
+    for (int j = 0; j < SynPlan<W>::K; ++j) P.d[j] = 0u;
+    if (w < 2 * nw) {
+        const bool zc = w >= nw;
+        const int ww = zc ? w - nw : w;
+        P.w = w;
+        P.writer = sub == 0;
+        const int valid = l - 32 * ww;
+        P.mask = valid >= 32 ? 0xffffffffu : ((1u << valid) - 1u);
+#pragma unroll
+        for (int j = 0; j < SynPlan<W>::K; ++j) {
+            const int k = sub + j * lpw;
+            if (k < 2 * W) {
+                const bool left = k < W;
+                const int e = gm.gbexp[(left != zc) ? k % W : 8 + k % W];
+                int start = 32 * ww + (zc ? l - e : e);
+                start = start >= l ? start - l : start;
+                start = start >= l ? start - l : start;
+                const int blk = left ? (zc ? kXL : kZL) : (zc ? kXR : kZR);
+                const uint32_t b0 = (uint32_t)(blk * (nw + 1));
+                const uint32_t n1 = (uint32_t)(l - start);
+                P.d[j] = (b0 + (uint32_t)(start >> 5)) | (b0 << 10) | ((uint32_t)(start & 31) << 20) |
+                         ((n1 < 32u ? n1 : 0u) << 25) | 0x80000000u;
+            }
+        }
+    }
+    return P;
+}
+
+template <int W, int T>
+__device__ __forceinline__ int circ_syndrome_plan(const SynPlan<W> &P, const GroupMem &gm, const uint32_t *base,
+                                                  uint32_t *out, int lpw)
+{
+    uint32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < SynPlan<W>::K; ++j) {
+        const uint32_t d = P.d[j];
+        if (d & 0x80000000u) {
+            const uint32_t *B = gm.bits + (d & 0x3ffu);
+            uint32_t x = __funnelshift_r(B[0], B[1], d >> 20);
+            const uint32_t n1 = (d >> 25) & 31u;
+            if (n1) x |= gm.bits[(d >> 10) & 0x3ffu] << n1;
+            acc ^= x;
+        }
+    }
+    acc ^= __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc ^= __shfl_xor_sync(0xffffffffu, acc, 2);
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1)
+        if (o < lpw) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
+    int cnt = 0;
+    if (P.writer) {
+        const uint32_t v = ((base ? base[P.w] : 0u) ^ acc) & P.mask;
+        out[P.w] = v;
+        cnt = __popc(v);
+    }
+    return cnt;
+}
+
 // Pack per-qubit Pauli codes (bytes in gm.ehat scratch) into the bitmaps.
 template <int T>
 __device__ __forceinline__ void bitmaps_from_bytes(const KParams &p, const GroupMem &gm, const uint8_t *e, int tid)
@@ -550,11 +633,12 @@ template <int W, bool ADD>
 __device__ __forceinline__ uint32_t vn_update_fixed(unsigned char *col, uint32_t rowb, float l0, float kapc)
 {
     constexpr int D = 2 * W;
+    const uint32_t cs = smem_addr(col);
     float c[D];
     OptF ox[D], oz[D], oa[D];
 #pragma unroll
     for (int s = 0; s < D; ++s) {
-        c[s] = lds_f(col, s * rowb);
+        c[s] = lds_a(cs + s * rowb);
         // anti_X keeps Z-edges (z-bit), anti_Z keeps X-edges (x-bit)
         ox[s] = OptF{c[s], s >= W};
         oz[s] = OptF{c[s], s < W};
@@ -567,14 +651,14 @@ __device__ __forceinline__ uint32_t vn_update_fixed(unsigned char *col, uint32_t
     const float bY = l0 + tY;
     if constexpr (ADD) {
 #pragma unroll
-        for (int s = 0; s < D; ++s) sts_u(col, s * rowb, f2u(l0 + (tY - c[s])));  // clipped by the consumer
+        for (int s = 0; s < D; ++s) sts_a(cs + s * rowb, f2u(l0 + (tY - c[s])));  // clipped by the consumer
     } else {
         // X-edge: self X, anti {Z, Y}; Z-edge: self Z, anti {X, Y}; no Y
         // edges, so V[X] = b_Z + F(S_Z), V[Z] = b_X + F(S_X) (vn_F)
         const float vX = bZ + vn_F(sZ, kapc);
         const float vZ = bX + vn_F(sX, kapc);
 #pragma unroll
-        for (int s = 0; s < D; ++s) sts_u(col, s * rowb, f2u((s < W ? vX : vZ) - c[s]));  // clipped by the consumer
+        for (int s = 0; s < D; ++s) sts_a(cs + s * rowb, f2u((s < W ? vX : vZ) - c[s]));  // clipped by the consumer
     }
     return hard_decision(bX, bZ, bY);
 }
@@ -733,6 +817,12 @@ __global__ void __launch_bounds__(640) decode_kernel(const KParams p)
 
     // hard decision with all-zero check messages: argmin(0, L0, L0, L0)
     const uint32_t hd0 = hard_decision(p.l0, p.l0, p.l0);
+    // bicycle residual plan (loop-invariant syndrome windows), lpw >= 4
+    const bool use_plan = W > 0 && p.lpw >= 4;
+    SynPlan<(W > 0 ? W : 1)> plan;
+    if constexpr (W > 0) {
+        if (use_plan) plan = syn_plan<W, T>(p, gm, tid);
+    }
     const bool capture = p.tr_vn != nullptr || p.tr_cn != nullptr;
 
     while (true) {
@@ -836,7 +926,8 @@ __global__ void __launch_bounds__(640) decode_kernel(const KParams p)
             uint32_t res = 0;
             int part;
             if constexpr (W > 0) {
-                part = circ_syndrome<W, T>(p, gm, gm.synw, gm.resw, tid);
+                part = use_plan ? circ_syndrome_plan<W, T>(plan, gm, gm.synw, gm.resw, p.lpw)
+                                : circ_syndrome<W, T>(p, gm, gm.synw, gm.resw, tid);
             } else {
                 res = syn_bits ^ syndrome_bits_generic<T>(p, gm, tid);
                 part = __popc(res);
