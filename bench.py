@@ -268,48 +268,48 @@ def run_ours(args, rank, world, local_rank):
         return h_syn, h_words
 
     hosts = {p: host_syndromes(p) for p in PS}
-    d_syn = torch.empty((FRAMES_PER_POINT, g.m), dtype=torch.uint8, device=dev)
-    d_words = torch.empty(hosts[PS[0]][1].shape, dtype=torch.int32, device=dev)
     h_out = torch.empty((len(points), 9 * FRAMES_PER_POINT), dtype=torch.uint8, pin_memory=True)
 
+    h_outs = [(h_out[k, 8 * FRAMES_PER_POINT:], h_out[k, : 8 * FRAMES_PER_POINT].view(torch.int64))
+              for k in range(len(points))]
+
     def e2e_run(packed):
+        # decode_host_batches: H2D of point k+1 overlaps the decode of point k
+        # (side stream, double buffer); results land in pinned host memory
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        h2d = d2h = 0
-        for k, (name, cfg, p) in enumerate(points):
-            if packed:
-                d_words.copy_(hosts[p][1], non_blocking=True)
-                h2d += hosts[p][1].numel() * 4
-                out = P.decode_batch_packed_device(dg, d_words, P.prior_llr(p).llr, cfg)
-            else:
-                d_syn.copy_(hosts[p][0], non_blocking=True)
-                h2d += hosts[p][0].numel()
-                out = P.decode_batch_device(dg, d_syn, P.prior_llr(p).llr, cfg, e_hat=False)
-            h_out[k, : 8 * FRAMES_PER_POINT].view(torch.int64).copy_(out["iterations"], non_blocking=True)
-            h_out[k, 8 * FRAMES_PER_POINT:].copy_(out["success"], non_blocking=True)
-            d2h += 9 * FRAMES_PER_POINT
-        torch.cuda.synchronize()
+        batches = [P.HostBatch(hosts[p][1] if packed else hosts[p][0], P.prior_llr(p).llr, cfg, packed=packed)
+                   for name, cfg, p in points]
+        P.decode_host_batches(dg, batches, device=dev, outputs=h_outs)
         ms = (time.perf_counter() - t0) * 1e3
+        h2d = sum(b.syndromes.numel() * b.syndromes.element_size() for b in batches)
+        d2h = 9 * FRAMES_PER_POINT * len(points)
         if world > 1:
             t = torch.tensor([ms], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms, h2d, d2h
 
+    # the _decode_frames drop-in (inputs are (seed, start, count) only; one
+    # untimed pass, then the median of up to 3)
+    def frames_run():
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for name, cfg, p in points:
+            P.decode_frames(dg, cfg, p, p, SEED, base, FRAMES_PER_POINT)
+        return (time.perf_counter() - t0) * 1e3
+
+    frames_run()
+    frames_ms = statistics.median(frames_run() for _ in range(max(1, min(args.steps, 3))))
+    e2e_run(False)  # untimed: first-touch of the pinned outputs and device buffers
     e2e_runs = [e2e_run(False) for _ in range(max(1, args.steps))]
     e2e_ms = statistics.median(r[0] for r in e2e_runs)
     e2e_value = frames_step / (e2e_ms / 1e3)
     e2e_h2d, e2e_d2h = e2e_runs[0][1] * world, e2e_runs[0][2] * world
     packed_runs = [e2e_run(True) for _ in range(max(1, min(args.steps, 3)))]
     packed_ms = statistics.median(r[0] for r in packed_runs)
-    # the _decode_frames drop-in (inputs are (seed, start, count) only)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for name, cfg, p in points:
-        P.decode_frames(dg, cfg, p, p, SEED, base, FRAMES_PER_POINT)
-    frames_ms = (time.perf_counter() - t0) * 1e3
     # the e2e decodes must agree with the device-timed step (same frames)
     if world == 1:
         assert int(h_out[:, 8 * FRAMES_PER_POINT:].sum()) == int(cnt[:, 0].sum() - cnt[:, 1].sum())
@@ -370,12 +370,13 @@ def run_ours(args, rank, world, local_rank):
                      "share_of_step": share},
         "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": int(e2e_h2d),
                 "d2h_bytes_per_step": int(e2e_d2h),
-                "api": "decode_batch_device: uint8 syndromes (reference decode_batch format) from pinned host "
-                       "memory -> device -> success + iterations back to pinned host, every point of the step"},
+                "api": "decode_host_batches: uint8 syndromes (reference decode_batch format) in pinned host "
+                       "memory -> device (H2D of point k+1 overlapping the decode of point k) -> success + "
+                       "iterations back to pinned host, every point of the step"},
         "e2e_packed": {"value": frames_step / (packed_ms / 1e3), "unit": "frames/s",
                        "h2d_bytes_per_step": int(packed_runs[0][1] * world),
                        "d2h_bytes_per_step": int(packed_runs[0][2] * world),
-                       "api": "decode_batch_packed_device: bit-packed syndromes (32 B/frame)"},
+                       "api": "decode_host_batches(packed): bit-packed syndromes (32 B/frame)"},
         "e2e_frames": {"value": frames_step / world / (frames_ms / 1e3) * world, "unit": "frames/s",
                        "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 9 * FRAMES_PER_POINT * len(points) * world,
                        "api": "decode_frames, the qsagms.harness._decode_frames drop-in (inputs are seed/start/count; "

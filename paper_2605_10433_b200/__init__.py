@@ -49,6 +49,7 @@ from .decoder import (  # noqa: E402
     syndrome_ratio,
 )
 from . import dist  # noqa: E402,F401
+from .stream import HostBatch, decode_host_batches  # noqa: E402
 from .device import DeviceGraph, device_graph  # noqa: E402
 from .harness import (  # noqa: E402
     FerPoint,
@@ -76,4 +77,5 @@ __all__ = [
     "effective_gain", "syndrome_ratio", "DeviceGraph", "device_graph",
     "FerPoint", "SweepConfig", "config_digest", "decode_frames", "decode_frames_device",
     "install", "run_point", "run_sweep", "wilson_interval", "build_gb_graph", "tanner_graph",
+    "HostBatch", "decode_host_batches",
 ]

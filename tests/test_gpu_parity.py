@@ -215,3 +215,24 @@ def test_full_occupancy_runs_are_deterministic(P, spec, variant):
     runs = [P.decode_frames_device(g, cfg, 0.08, 0.08, 0, 0, 1 << 20) for _ in range(3)]
     for f, it, _ in runs[1:]:
         assert torch.equal(f, runs[0][0]) and torch.equal(it, runs[0][1])
+
+
+def test_decode_host_batches_pipeline(P, oracle):
+    """decode_host_batches (overlapped H2D / decode, double buffer) returns
+    exactly what decode_batch returns per batch, for byte and packed
+    syndromes and mixed decoders."""
+    g = P.gb_graph(P.GbSpec(*GB254))
+    batches, want = [], []
+    for k, (variant, kw) in enumerate(CFGS):
+        eps = 0.04 + 0.02 * k
+        e = oracle.sample_errors(g.n, eps, 11, 1000 * k, 700 + 50 * k)
+        syn = oracle.syndromes_of(g, e)
+        cfg = _cfg(P, variant, kw, l_max=40)
+        want.append(P.decode_batch(g, syn, P.prior_llr(eps), cfg))
+        packed = k % 2 == 1
+        host = torch.from_numpy(P.pack_syndromes(syn).view(np.int32) if packed else syn).pin_memory()
+        batches.append(P.HostBatch(host, P.prior_llr(eps).llr, cfg, packed=packed))
+    got = P.decode_host_batches(g, batches)
+    for (succ, iters), w in zip(got, want):
+        assert np.array_equal(succ.numpy().astype(bool), w.success)
+        assert np.array_equal(iters.numpy(), w.iterations)
