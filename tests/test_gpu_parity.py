@@ -236,3 +236,20 @@ def test_decode_host_batches_pipeline(P, oracle):
     for (succ, iters), w in zip(got, want):
         assert np.array_equal(succ.numpy().astype(bool), w.success)
         assert np.array_equal(iters.numpy(), w.iterations)
+
+
+@pytest.mark.parametrize("ell,w", [(160, 5), (600, 4)])
+def test_unplanned_syndrome_shapes_bit_exact(P, oracle, ell, w):
+    """Bicycle shapes with fewer than 4 lanes per syndrome word (l = 160 on
+    one warp, l = 600 on 128 threads) take the generic circ_syndrome path
+    instead of the per-lane window plan; both must match the oracle."""
+    spec = P.random_gb_spec(ell, w, seed=1)
+    g = P.gb_graph(spec)
+    assert g.kind == w
+    for variant, kw in CFGS:
+        cfg = _cfg(P, variant, kw, l_max=25)
+        fails, iters, ehat = P.decode_frames_device(g, cfg, 0.07, 0.07, 3, 0, 64, want_ehat=True)
+        of, oi, oe, _ = oracle.frames(g, cfg, 0.07, 0.07, 3, 0, 64, want_ehat=True)
+        assert np.array_equal(fails.cpu().numpy().astype(bool), of), variant
+        assert np.array_equal(iters.cpu().numpy(), oi), variant
+        assert np.array_equal(ehat.cpu().numpy(), oe), variant
