@@ -52,7 +52,8 @@ def decoders(P):
 def workload_desc():
     return ("configs[1]: [[254,28]] GB (l=127) sweep p in {0.02,0.04,0.06,0.08,0.10} x "
             "{BP4, SMS a in {0.5,0.625,0.75,0.875,1.0}, SAGMS(0.30,0.50,1.10)}, "
-            "2^20 frames/point/GPU, l_max=100, fp32, marginal VN, seed 0")
+            + ("2^20" if FRAMES_PER_POINT == 1 << 20 else str(FRAMES_PER_POINT))
+            + " frames/point/GPU, l_max=100, fp32, marginal VN, seed 0")
 
 
 class ClockSampler:
