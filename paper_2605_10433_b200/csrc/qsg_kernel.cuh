@@ -37,6 +37,7 @@
 #include <stdint.h>
 
 #include "qsg_math.cuh"
+#include "qsg_math2.cuh"
 #include "qsg_philox.cuh"
 
 namespace qsg {
@@ -496,12 +497,20 @@ __device__ __forceinline__ void cn_update_fixed(const uint16_t *row, uint32_t ms
             x[k] = fmaxf(fminf(fabsf(v[k]), kClip), 1e-12f);
             xmin = fminf(xmin, x[k]);
         }
+        // phi on edge pairs (k, k+1): FFMA2 / FADD2 / FMUL2 (qsg_math2.cuh)
+        static_assert(D % 2 == 0, "bicycle checks have even degree");
         if (__all_sync(act, xmin >= kLn2f)) {
 #pragma unroll
-            for (int k = 0; k < D; ++k) ph[k] = phi_hi(x[k]);
+            for (int k = 0; k < D; k += 2) {
+                const F2 y = phi_hi2(pk(x[k], x[k + 1]));
+                ph[k] = lo(y); ph[k + 1] = hi(y);
+            }
         } else {
 #pragma unroll
-            for (int k = 0; k < D; ++k) ph[k] = phi(x[k]);
+            for (int k = 0; k < D; k += 2) {
+                const F2 y = phi2(pk(x[k], x[k + 1]));
+                ph[k] = lo(y); ph[k + 1] = hi(y);
+            }
         }
         OptF o[D];
 #pragma unroll
@@ -509,7 +518,11 @@ __device__ __forceinline__ void cn_update_fixed(const uint16_t *row, uint32_t ms
         const float total = segsum_c<D>(o);
         float r[D];
 #pragma unroll
-        for (int k = 0; k < D; ++k) r[k] = phi(fminf(fmaxf(total - ph[k], 1e-12f), 50.0f));
+        for (int k = 0; k < D; k += 2) {
+            const F2 e = sub2(bc(total), pk(ph[k], ph[k + 1]));
+            const F2 y = phi2(pk(fminf(fmaxf(lo(e), 1e-12f), 50.0f), fminf(fmaxf(hi(e), 1e-12f), 50.0f)));
+            r[k] = lo(y); r[k + 1] = hi(y);
+        }
 #pragma unroll
         for (int k = 0; k < D; ++k) sts_a(ad[k], (f2u(v[k]) & 0x80000000u) ^ f2u(fminf(r[k], kClip)) ^ sgn);
     } else {
@@ -655,10 +668,14 @@ __device__ __forceinline__ uint32_t vn_update_fixed(unsigned char *col, uint32_t
     } else {
         // X-edge: self X, anti {Z, Y}; Z-edge: self Z, anti {X, Y}; no Y
         // edges, so V[X] = b_Z + F(S_Z), V[Z] = b_X + F(S_X) (vn_F)
-        const float vX = bZ + vn_F(sZ, kapc);
-        const float vZ = bX + vn_F(sX, kapc);
+        // both factors at once (FFMA2 / FADD2 / FMUL2, qsg_math2.cuh)
+        const F2 v2 = add2(pk(bZ, bX), vn_F2(sZ, sX, bc(kapc)));
 #pragma unroll
-        for (int s = 0; s < D; ++s) sts_a(cs + s * rowb, f2u((s < W ? vX : vZ) - c[s]));  // clipped by the consumer
+        for (int s = 0; s < W; ++s) {  // X-edge s and Z-edge W + s together
+            const F2 o2 = sub2(v2, pk(c[s], c[W + s]));
+            sts_a(cs + s * rowb, f2u(lo(o2)));  // clipped by the consumer
+            sts_a(cs + (W + s) * rowb, f2u(hi(o2)));
+        }
     }
     return hard_decision(bX, bZ, bY);
 }
