@@ -516,12 +516,36 @@ __device__ __forceinline__ void cn_update_fixed(const uint16_t *row, uint32_t ms
 #pragma unroll
         for (int k = 0; k < D; ++k) o[k] = OptF{ph[k], true};
         const float total = segsum_c<D>(o);
-        float r[D];
+        float r[D], ex[D];
+        float emin = 50.0f, emax = 0.0f;
 #pragma unroll
         for (int k = 0; k < D; k += 2) {
             const F2 e = sub2(bc(total), pk(ph[k], ph[k + 1]));
-            const F2 y = phi2(pk(fminf(fmaxf(lo(e), 1e-12f), 50.0f), fminf(fmaxf(hi(e), 1e-12f), 50.0f)));
-            r[k] = lo(y); r[k + 1] = hi(y);
+            ex[k] = fminf(fmaxf(lo(e), 1e-12f), 50.0f);
+            ex[k + 1] = fminf(fmaxf(hi(e), 1e-12f), 50.0f);
+            emin = fminf(emin, fminf(ex[k], ex[k + 1]));
+            emax = fmaxf(emax, fmaxf(ex[k], ex[k + 1]));
+        }
+        // extrinsic phi: one side only when the whole warp is there (most
+        // warps at low p sit below ln 2), else both sides (paired)
+        if (__all_sync(act, emax < kLn2f)) {
+#pragma unroll
+            for (int k = 0; k < D; k += 2) {
+                const F2 y = phi_lo2(pk(ex[k], ex[k + 1]));
+                r[k] = lo(y); r[k + 1] = hi(y);
+            }
+        } else if (__all_sync(act, emin >= kLn2f)) {
+#pragma unroll
+            for (int k = 0; k < D; k += 2) {
+                const F2 y = phi_hi2(pk(ex[k], ex[k + 1]));
+                r[k] = lo(y); r[k + 1] = hi(y);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < D; k += 2) {
+                const F2 y = phi2(pk(ex[k], ex[k + 1]));
+                r[k] = lo(y); r[k + 1] = hi(y);
+            }
         }
 #pragma unroll
         for (int k = 0; k < D; ++k) sts_a(ad[k], (f2u(v[k]) & 0x80000000u) ^ f2u(fminf(r[k], kClip)) ^ sgn);
