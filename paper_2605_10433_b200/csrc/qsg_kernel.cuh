@@ -19,10 +19,17 @@
 // separated by group barriers).  Slot of the s-th edge of qubit j (qubit
 // order = ascending check index, code.py:171) is s * n_pad + j, so qubit
 // reads/writes are unit-stride across the group (conflict-free).  Checks
-// reach their edges through a per-graph table of byte offsets, one row of
-// `row_words` (odd, so rows start in distinct banks) u32 words per check:
-// entries 0..d-1 in canonical order (the order of the BP4 phi sum) and an
-// info word at index dc_max.  Hard decisions are kept as one u32 per qubit.
+// reach their edges through a per-graph table, one row of `row_words` (odd,
+// so rows start in distinct banks) u32 words per check: generic rows hold
+// byte offsets (+ the edge symbol) in canonical order and an info word at
+// index dc_max; bicycle rows hold u16 slot indices, in canonical order for
+// BP4 (the order of its phi sum) and in exponent order for the order-free
+// min-sum update (consecutive checks -> consecutive qubits, few bank
+// conflicts).  Generic kernels keep hard decisions as one u32 per qubit.
+//
+// The fp32 recipes (qsg_math.cuh) run scalar or, where two independent
+// evaluations exist, paired on FFMA2 / FADD2 / FMUL2 (qsg_math2.cuh) with
+// bit-identical results.
 //
 // W > 0 selects the generalized-bicycle specialisation (circulant A, B with
 // |a| = |b| = W, code.py:201-231): degrees, masks and numpy's pairwise
@@ -212,11 +219,13 @@ struct GroupMem {
 
 enum { kXL = 0, kZL = 1, kXR = 2, kZR = 3 };
 
-// ---- ALU-pipe relief -------------------------------------------------------
-// The bicycle kernels are bound by the half-rate ALU pipe (FMNMX / FSETP /
-// FSEL / LOP3 / PRMT); these helpers pin cheaper forms: a plain 16-bit shared
-// load (no PRMT unpacking of paired entries) and a single three-input LUT
-// for the sign merge (the compiler otherwise splits it in two).
+// ---- check-phase helpers ---------------------------------------------------
+// The check phase is bound by the half-rate ALU pipe (FMNMX / FSETP / SEL /
+// LOP3) and by issue; these helpers pin the cheapest forms: a plain 16-bit
+// shared load (no PRMT unpacking of paired entries) and a single
+// three-input LUT for the sign merge (the compiler otherwise splits it in
+// two).  Moving the sign merge to the FMA pipe (IMAD.HI + IMAD) measured 5%
+// slower: the extra issue slot costs more than the ALU relief.
 __device__ __forceinline__ uint32_t lds_u16(const uint16_t *p)
 {
     uint32_t v;
