@@ -1,0 +1,81 @@
+// Paired (f32x2) vs scalar recipes on the device, bit for bit (dev tool):
+// every qsg_math2.cuh function against two calls of its qsg_math.cuh
+// counterpart on 5e5 argument pairs; the raw "sub_add" cases show ptxas
+// contracting an f32x2 multiply into a following add (why the recipes fuse
+// those steps explicitly).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -fmad=false -std=c++17 -o /tmp/pc tools/pair_check.cu && /tmp/pc
+#include <cstdio>
+#include <cstdint>
+#include <cstring>
+#include <cmath>
+#include "../paper_2605_10433_b200/csrc/qsg_math2.cuh"
+using namespace qsg;
+__global__ void k(const float* x, float* o, int n, int which) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (2 * i + 1 >= n) return;
+  float a = x[2 * i], b = x[2 * i + 1];
+  float s0, s1, p0, p1;
+  F2 r;
+  switch (which) {
+    case 0: s0 = exp_neg(a); s1 = exp_neg(b); r = exp_neg2(pk(a, b)); break;
+    case 1: s0 = log1p_01(a); s1 = log1p_01(b); r = log1p_01_2(pk(a, b)); break;
+    case 2: s0 = log_pos(a); s1 = log_pos(b); r = log_pos2(pk(a, b)); break;
+    case 3: s0 = vn_F(a, 0.03f); s1 = vn_F(b, 0.03f); r = vn_F2(a, b, bc(0.03f)); break;
+    case 4: s0 = phi_hi(a); s1 = phi_hi(b); r = phi_hi2(pk(a, b)); break;
+    case 5: s0 = phi_lo(a); s1 = phi_lo(b); r = phi_lo2(pk(a, b)); break;
+    case 6: s0 = phi(a); s1 = phi(b); r = phi2(pk(a, b)); break;
+    case 7: { // H(v) poly only
+      float v0 = a * a, v1 = b * b;
+      float H0 = -2.4306313e-05f; H0 = fmaf(H0, v0, 0.0003411371f); H0 = fmaf(H0, v0, -0.0048610563f); H0 = fmaf(H0, v0, 0.083333336f);
+      float H1 = -2.4306313e-05f; H1 = fmaf(H1, v1, 0.0003411371f); H1 = fmaf(H1, v1, -0.0048610563f); H1 = fmaf(H1, v1, 0.083333336f);
+      s0 = H0; s1 = H1;
+      F2 v = mul2(pk(a, b), pk(a, b));
+      F2 H = fma2(bc(-2.4306313e-05f), v, bc(0.0003411371f)); H = fma2(H, v, bc(-0.0048610563f)); H = fma2(H, v, bc(0.083333336f));
+      r = H; break; }
+    case 8: { // x*x * H-ish product and difference
+      s0 = (kLn2f - a) + a * b; s1 = (kLn2f - b) + b * a;
+      { F2 d = sub2(bc(kLn2f), pk(a, b)), m = mul2(pk(a, b), pk(b, a));
+        F2 rr; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rr.v) : "l"(m.v), "l"(bc(1.0f).v), "l"(d.v)); r = rr; }
+      break; }
+    case 10: s0 = a * b; s1 = b * (a + 1.0f); r = mul2(pk(a, b), pk(b, a + 1.0f)); break;
+    case 11: s0 = a + b; s1 = b + (a * 0.5f); r = add2(pk(a, b), pk(b, a * 0.5f)); break;
+    case 12: s0 = kLn2f - a; s1 = kLn2f - b; r = sub2(bc(kLn2f), pk(a, b)); break;
+    case 13: { float m0 = a * b, m1 = b * (a + 1.0f); s0 = (kLn2f - a) + m0; s1 = (kLn2f - b) + m1;
+               F2 m = mul2(pk(a, b), pk(b, a + 1.0f)); r = add2(sub2(bc(kLn2f), pk(a, b)), m); break; }
+    case 9: { // plain fma with broadcast immediate
+      s0 = fmaf(a, 0.0003411371f, b); s1 = fmaf(b, 0.0003411371f, a);
+      r = fma2(pk(a, b), bc(0.0003411371f), pk(b, a)); break; }
+    default: s0 = s1 = 0.0f; r = pk(0.0f, 0.0f); break;
+  }
+  p0 = lo(r); p1 = hi(r);
+  o[4 * i] = s0; o[4 * i + 1] = s1; o[4 * i + 2] = p0; o[4 * i + 3] = p1;
+}
+int main() {
+  const int n = 1 << 20;
+  float *h = new float[n], *ho = new float[2 * n];
+  float *d, *dout; cudaMalloc(&d, n * 4); cudaMalloc(&dout, 2 * n * 4);
+  const char* names[] = {"exp_neg", "log1p_01", "log_pos", "vn_F", "phi_hi", "phi_lo", "phi", "Hpoly", "sub_add", "fma_imm", "mul", "add", "subc", "sub_add2"};
+  for (int w = 0; w < 14; ++w) {
+    srand(1);
+    for (int i = 0; i < n; ++i) {
+      float u = rand() / (float)RAND_MAX;
+      if (w == 0) h[i] = -87.0f * u;
+      else if (w == 1) h[i] = u;
+      else if (w == 2) h[i] = powf(10.0f, -30.0f + 32.0f * u);
+      else if (w == 3) h[i] = -200.0f + 400.0f * u;
+      else if (w <= 6) h[i] = powf(10.0f, -12.0f + 13.8f * u);
+      else h[i] = -3.0f + 6.0f * u;
+    }
+    cudaMemcpy(d, h, n * 4, cudaMemcpyHostToDevice);
+    k<<<n / 2 / 256, 256>>>(d, dout, n, w);
+    cudaMemcpy(ho, dout, 2 * n * 4, cudaMemcpyDeviceToHost);
+    int bad = 0;
+    for (int i = 0; i < n / 2; ++i) {
+      uint32_t a, b, c, e;
+      memcpy(&a, &ho[4 * i], 4); memcpy(&b, &ho[4 * i + 1], 4); memcpy(&c, &ho[4 * i + 2], 4); memcpy(&e, &ho[4 * i + 3], 4);
+      if (a != c || b != e) { if (bad < 3) printf("  %s x=(%g,%g) scalar=(%.9g,%.9g) paired=(%.9g,%.9g)\n", names[w], h[2*i], h[2*i+1], ho[4*i], ho[4*i+1], ho[4*i+2], ho[4*i+3]); ++bad; }
+    }
+    printf("%s mismatches %d / %d\n", names[w], bad, n / 2);
+  }
+  return 0;
+}
