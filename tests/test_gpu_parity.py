@@ -10,6 +10,7 @@ The bar ("Numerics contract"):
 from __future__ import annotations
 
 import hashlib
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -253,3 +254,17 @@ def test_unplanned_syndrome_shapes_bit_exact(P, oracle, ell, w):
         assert np.array_equal(fails.cpu().numpy().astype(bool), of), variant
         assert np.array_equal(iters.cpu().numpy(), oi), variant
         assert np.array_equal(ehat.cpu().numpy(), oe), variant
+
+
+def test_paired_recipes_equal_scalar_on_device(tmp_path):
+    """tools/pair_check.cu: every paired (FFMA2/FADD2/FMUL2) recipe of
+    qsg_math2.cuh equals two calls of its scalar qsg_math.cuh counterpart
+    bit for bit on 5e5 argument pairs per function, on the device."""
+    import subprocess
+    root = Path(__file__).resolve().parents[1]
+    exe = tmp_path / "pair_check"
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-fmad=false", "-std=c++17",
+                    "-o", str(exe), str(root / "tools" / "pair_check.cu")], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    assert "RECIPE_MISMATCHES 0" in out.stdout, out.stdout[-2000:]
+    assert out.returncode == 0

@@ -55,6 +55,7 @@ int main() {
   float *h = new float[n], *ho = new float[2 * n];
   float *d, *dout; cudaMalloc(&d, n * 4); cudaMalloc(&dout, 2 * n * 4);
   const char* names[] = {"exp_neg", "log1p_01", "log_pos", "vn_F", "phi_hi", "phi_lo", "phi", "Hpoly", "sub_add", "fma_imm", "mul", "add", "subc", "sub_add2"};
+  int recipe_bad = 0;
   for (int w = 0; w < 14; ++w) {
     srand(1);
     for (int i = 0; i < n; ++i) {
@@ -76,6 +77,8 @@ int main() {
       if (a != c || b != e) { if (bad < 3) printf("  %s x=(%g,%g) scalar=(%.9g,%.9g) paired=(%.9g,%.9g)\n", names[w], h[2*i], h[2*i+1], ho[4*i], ho[4*i+1], ho[4*i+2], ho[4*i+3]); ++bad; }
     }
     printf("%s mismatches %d / %d\n", names[w], bad, n / 2);
+    if (w != 8 && w != 13) recipe_bad += bad;  // 8, 13: raw mul+add, contracted by ptxas on purpose
   }
-  return 0;
+  printf("RECIPE_MISMATCHES %d\n", recipe_bad);
+  return recipe_bad != 0;
 }
