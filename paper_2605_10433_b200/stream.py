@@ -31,6 +31,17 @@ class HostBatch:
     packed: bool = False
 
 
+_COPY_STREAMS: dict = {}
+
+
+def _copy_stream(dev: torch.device) -> torch.cuda.Stream:
+    """One side stream per device for the host-to-device copies."""
+    s = _COPY_STREAMS.get(dev.index)
+    if s is None:
+        s = _COPY_STREAMS[dev.index] = torch.cuda.Stream(dev)
+    return s
+
+
 def decode_host_batches(graph, batches, *, device=None, early_stop: bool = True, outputs=None):
     """Decode ``batches`` (an iterable of HostBatch) with copy/compute overlap.
 
@@ -42,7 +53,8 @@ def decode_host_batches(graph, batches, *, device=None, early_stop: bool = True,
     dev = require_cuda(device)
     dg = device_graph(graph, dev)
     comp = torch.cuda.current_stream(dev)
-    copy = torch.cuda.Stream(dev)
+    copy = _copy_stream(dev)
+    copy.wait_stream(comp)  # buffers from earlier work on the caller's stream
     bufs: dict = {}
     ready = [torch.cuda.Event(), torch.cuda.Event()]
     free = [None, None]
