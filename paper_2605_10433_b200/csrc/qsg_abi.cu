@@ -358,7 +358,7 @@ int launch_decode(qsg_graph *g, const qsg_decoder_cfg *cfg, qsg::KParams &p, cud
 {
     const bool bp4 = cfg->variant == QSG_BP4, add = cfg->vn_mode == QSG_VN_ADDITIVE;
     if (!bp4 && g->d_cn_tab_x) p.cn_tab = g->d_cn_tab_x;
-    void *fn = qsg::kernel_ptr(g->kind, g->threads, bp4, add);
+    void *fn = qsg::kernel_ptr(g->kind, g->threads, bp4, add, g->n_pad);
     if (!fn) return fail(QSG_EUNSUPPORTED, "no kernel for this graph kind");
     qsg::LaunchCfg lc;
     int rc = launch_cfg(g, bp4, add, fn, &lc);
@@ -468,16 +468,16 @@ int create_common(int32_t device, qsg_graph **out, qsg_graph **g)
 }  // namespace
 
 namespace qsg {
-void *kernel_ptr(int W, int T, bool bp4, bool additive)
+void *kernel_ptr(int W, int T, bool bp4, bool additive, int np)
 {
     switch (W) {
-    case 0: return kernel_ptr_w0(T, bp4, additive);
-    case 2: return kernel_ptr_w2(T, bp4, additive);
-    case 3: return kernel_ptr_w3(T, bp4, additive);
-    case 4: return kernel_ptr_w4(T, bp4, additive);
-    case 5: return kernel_ptr_w5(T, bp4, additive);
-    case 6: return kernel_ptr_w6(T, bp4, additive);
-    case 8: return kernel_ptr_w8(T, bp4, additive);
+    case 0: return kernel_ptr_w0(T, bp4, additive, np);
+    case 2: return kernel_ptr_w2(T, bp4, additive, np);
+    case 3: return kernel_ptr_w3(T, bp4, additive, np);
+    case 4: return kernel_ptr_w4(T, bp4, additive, np);
+    case 5: return kernel_ptr_w5(T, bp4, additive, np);
+    case 6: return kernel_ptr_w6(T, bp4, additive, np);
+    case 8: return kernel_ptr_w8(T, bp4, additive, np);
     default: return nullptr;
     }
 }

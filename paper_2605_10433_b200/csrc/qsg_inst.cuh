@@ -8,17 +8,22 @@
 
 namespace qsg {
 
-template <int T>
+template <int T, int NP>
 static void *pick(bool bp4, bool add)
 {
-    if (bp4) return add ? (void *)decode_kernel<QSG_W, T, true, true> : (void *)decode_kernel<QSG_W, T, true, false>;
-    return add ? (void *)decode_kernel<QSG_W, T, false, true> : (void *)decode_kernel<QSG_W, T, false, false>;
+    if (bp4) return add ? (void *)decode_kernel<QSG_W, T, true, true, NP> : (void *)decode_kernel<QSG_W, T, true, false, NP>;
+    return add ? (void *)decode_kernel<QSG_W, T, false, true, NP> : (void *)decode_kernel<QSG_W, T, false, false, NP>;
 }
 
-void *QSG_FN(QSG_W)(int T, bool bp4, bool add)
+// np: compile-time qubit stride for the bicycle one-warp kernels at n_pad =
+// 256 (every l in (64, 128], the BASELINE codes); 0 = run-time stride.
+void *QSG_FN(QSG_W)(int T, bool bp4, bool add, int np)
 {
-    if (T == 32) return pick<32>(bp4, add);
-    if (T == 128) return pick<128>(bp4, add);
+#if QSG_W > 0
+    if (T == 32 && np == 256) return pick<32, 256>(bp4, add);
+#endif
+    if (T == 32) return pick<32, 0>(bp4, add);
+    if (T == 128) return pick<128, 0>(bp4, add);
     return nullptr;
 }
 

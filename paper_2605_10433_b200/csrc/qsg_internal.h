@@ -18,14 +18,14 @@ constexpr int kBicycleWs[] = {2, 3, 4, 5, 6, 8};
 constexpr int kThreadCounts[] = {32, 128};
 
 // Returns the __global__ function for (W, T, bp4, additive) or nullptr.
-void *kernel_ptr(int W, int T, bool bp4, bool additive);
-void *kernel_ptr_w0(int T, bool bp4, bool additive);
-void *kernel_ptr_w2(int T, bool bp4, bool additive);
-void *kernel_ptr_w3(int T, bool bp4, bool additive);
-void *kernel_ptr_w4(int T, bool bp4, bool additive);
-void *kernel_ptr_w5(int T, bool bp4, bool additive);
-void *kernel_ptr_w6(int T, bool bp4, bool additive);
-void *kernel_ptr_w8(int T, bool bp4, bool additive);
+void *kernel_ptr(int W, int T, bool bp4, bool additive, int np);
+void *kernel_ptr_w0(int T, bool bp4, bool additive, int np);
+void *kernel_ptr_w2(int T, bool bp4, bool additive, int np);
+void *kernel_ptr_w3(int T, bool bp4, bool additive, int np);
+void *kernel_ptr_w4(int T, bool bp4, bool additive, int np);
+void *kernel_ptr_w5(int T, bool bp4, bool additive, int np);
+void *kernel_ptr_w6(int T, bool bp4, bool additive, int np);
+void *kernel_ptr_w8(int T, bool bp4, bool additive, int np);
 
 struct LaunchCfg {
     int groups = 0;        // groups (frames in flight) per CTA

@@ -675,9 +675,12 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, u
 // computed once per qubit and symbol (the fp32 restatement's recipe; the
 // oracle's fp32 path uses the same factorisation, its fp64 path the
 // reference's literal per-edge form).  Returns the hard decision.
-template <int W, bool ADD>
+// NP > 0: the qubit stride n_pad is a compile-time constant, so the D column
+// loads / stores use immediate offsets from one base (no address IMADs).
+template <int W, bool ADD, int NP>
 __device__ __forceinline__ uint32_t vn_update_fixed(unsigned char *col, uint32_t rowb, float l0, float kapc)
 {
+    if constexpr (NP > 0) rowb = 4u * NP;
     constexpr int D = 2 * W;
     const uint32_t cs = smem_addr(col);
     float c[D];
@@ -713,7 +716,7 @@ __device__ __forceinline__ uint32_t vn_update_fixed(unsigned char *col, uint32_t
     return hard_decision(bX, bZ, bY);
 }
 
-template <int W, int T, bool BP4, bool ADD>
+template <int W, int T, bool BP4, bool ADD, int NP>
 __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, int tid)
 {
     const uint32_t rowb = (uint32_t)p.n_pad * 4;
@@ -729,11 +732,11 @@ __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, i
             uint32_t e2[2] = {0u, 0u};
             if (c < l) {
                 if constexpr (kUnrollPair<T, BP4>) {
-                    e2[0] = vn_update_fixed<W, ADD>(msg + 4 * c, rowb, l0, kapc);
-                    e2[1] = vn_update_fixed<W, ADD>(msg + 4 * (l + c), rowb, l0, kapc);
+                    e2[0] = vn_update_fixed<W, ADD, NP>(msg + 4 * c, rowb, l0, kapc);
+                    e2[1] = vn_update_fixed<W, ADD, NP>(msg + 4 * (l + c), rowb, l0, kapc);
                 } else {
 #pragma unroll 1
-                    for (int h = 0; h < 2; ++h) e2[h] = vn_update_fixed<W, ADD>(msg + 4 * (h * l + c), rowb, l0, kapc);
+                    for (int h = 0; h < 2; ++h) e2[h] = vn_update_fixed<W, ADD, NP>(msg + 4 * (h * l + c), rowb, l0, kapc);
                 }
             }
             const uint32_t eL = e2[0], eR = e2[1];
@@ -824,7 +827,7 @@ __device__ __forceinline__ uint8_t ehat_of(const KParams &p, const GroupMem &gm,
     }
 }
 
-template <int W, int T, bool BP4, bool ADD>
+template <int W, int T, bool BP4, bool ADD, int NP>
 __global__ void __launch_bounds__(640) decode_kernel(const KParams p)
 {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1011,7 +1014,7 @@ __global__ void __launch_bounds__(640) decode_kernel(const KParams p)
             cn_phase<W, T, BP4>(p, gm, syn_bits, res, g0, g1, tid);
             group_sync<T>(g);
             if (capture && p.tr_cn) snapshot<T>(p, gm.msg, p.tr_cn + (f * p.l_max + n_snap) * p.E, tid, false);
-            vn_phase<W, T, BP4, ADD>(p, gm, tid);
+            vn_phase<W, T, BP4, ADD, NP>(p, gm, tid);
             group_sync<T>(g);
             if (capture) {
                 if (p.tr_vn) snapshot<T>(p, gm.msg, p.tr_vn + (f * p.l_max + n_snap) * p.E, tid, true);
