@@ -365,7 +365,7 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": len(points) * args.steps,
         "roofline": {"bound": "issue", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gop/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "qsg::decode_kernel<5,32,false,false> (min-sum family, marginal VN)",
+                     "kernel": "qsg::decode_kernel<5,32,false,false,256> (min-sum family, marginal VN, n_pad 256)",
                      "ops_per_cn_edge_update": "SURVEY.md 8(d): SAGMS 34.3, SMS 34.0",
                      "peak_basis": "148 SMs x 128 lane-instr/clk x measured median SM clock",
                      "share_of_step": share},
