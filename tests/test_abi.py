@@ -120,3 +120,5 @@ def test_decode_without_gpu_fails_loudly():
         P.decode_frames(g, cfg, 0.1, 0.1, 0, 0, 4)
     with pytest.raises(RuntimeError):
         P.decode_batch(g, np.zeros((2, g.m), np.uint8), P.prior_llr(0.1), cfg)
+    with pytest.raises(RuntimeError):
+        P.decode_host_batches(g, [P.HostBatch(torch.zeros((2, g.m), dtype=torch.uint8), 1.0, cfg)])
