@@ -1,0 +1,44 @@
+"""Randomised GPU-vs-oracle stress (dev tool, needs a GPU): random GB codes
+(l, w) across every kernel shape, random decoders / p / l_max / seeds;
+outcomes, iterations and e_hat must match the fp32 oracle bit for bit."""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2605_10433_b200 as P  # noqa: E402
+from oracle import oracle  # noqa: E402
+
+rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
+cases = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+bad = 0
+for i in range(cases):
+    ell = int(rng.choice([33, 47, 63, 64, 96, 127, 128, 150, 191, 255, 300, 511, 512]))
+    w = int(rng.choice([2, 3, 4, 5, 6, 8]))
+    if w >= ell // 2:
+        continue
+    try:
+        spec = P.random_gb_spec(ell, w, seed=int(rng.integers(1 << 30)))
+    except Exception as exc:  # no k > 0 code found quickly
+        print("skip", ell, w, exc)
+        continue
+    g = P.gb_graph(spec)
+    variant = str(rng.choice(["bp4", "ms", "sms", "sagms"]))
+    kw = {"alpha": float(rng.choice([0.5, 0.75, 1.0]))} if variant == "sms" else {}
+    if variant == "sagms":
+        kw["gain"] = P.GainParams(0.3, 0.5, 1.1)
+    cfg = P.DecoderConfig(variant, l_max=int(rng.integers(1, 60)),
+                          vn_mode=str(rng.choice(["marginal", "additive"])), **kw)
+    p = float(rng.uniform(0.01, 0.14))
+    seed, start, count = int(rng.integers(1 << 40)), int(rng.integers(1 << 20)), int(rng.integers(1, 400))
+    f, it, eh = P.decode_frames_device(g, cfg, p, p, seed, start, count, want_ehat=True)
+    of, oi, oe, _ = oracle.frames(g, cfg, p, p, seed, start, count, want_ehat=True)
+    ok = (np.array_equal(f.cpu().numpy().astype(bool), of) and np.array_equal(it.cpu().numpy(), oi)
+          and np.array_equal(eh.cpu().numpy(), oe))
+    bad += not ok
+    print(f"{'ok ' if ok else 'BAD'} l={ell} w={w} kind={g.kind} {variant} {cfg.vn_mode} l_max={cfg.l_max} "
+          f"p={p:.3f} frames={count}", flush=True)
+print("STRESS_FAILURES", bad)
+sys.exit(1 if bad else 0)
