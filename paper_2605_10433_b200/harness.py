@@ -82,11 +82,19 @@ def decode_frames(graph, decoder_cfg, epsilon, epsilon0, seed, start, count):
     return f_h.numpy().astype(bool), it_h.numpy().copy()
 
 
-def install(harness_module) -> None:
+def install(harness_module, batch_frames: int | None = 1 << 20) -> None:
     """Route a reference harness module's FER loop through the GPU, e.g.
     ``install(qsagms.harness)``; run it with workers=1 (the GPU is the
-    parallelism)."""
+    parallelism).
+
+    ``batch_frames`` also sets the harness's ``BATCH_FRAMES`` (4096 by
+    default, harness.py:40-41: "has no effect on results, only on
+    scheduling"): a 4096-frame call is latency-bound on the GPU by its
+    slowest (l_max-iteration) frame, 2^20 frames fill all 148 SMs.  None
+    leaves it unchanged."""
     harness_module._decode_frames = globals()["decode_frames"]
+    if batch_frames is not None and hasattr(harness_module, "BATCH_FRAMES"):
+        harness_module.BATCH_FRAMES = int(batch_frames)
 
 
 # -- protocol (harness.py:44-158, 248-356) ----------------------------------------

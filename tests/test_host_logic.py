@@ -185,11 +185,14 @@ def test_install_routes_reference_harness(reference, monkeypatch, oracle):
         f, it, _, _ = oracle.frames(oracle.Graph(graph), dcfg, eps, eps0, seed, start, count, precision=64)
         return f, it
     monkeypatch.setattr(H, "decode_frames", unit)
+    monkeypatch.setattr(RH, "BATCH_FRAMES", RH.BATCH_FRAMES)  # restored after the test
     original = RH._decode_frames
     try:
         P.install(RH)
-        assert RH._decode_frames is H.decode_frames is unit
+        assert RH._decode_frames is H.decode_frames is unit and RH.BATCH_FRAMES == 1 << 20
         got = RH.run_point(Hm, g, cfg, 0.5)
+        P.install(RH, batch_frames=7)  # any batching gives the same point (harness.py:40)
+        got7 = RH.run_point(Hm, g, cfg, 0.5)
     finally:
         RH._decode_frames = original
-    assert calls and got == want and (got.frames, got.failures) == (56, 50)
+    assert calls and got == want == got7 and (got.frames, got.failures) == (56, 50)
