@@ -63,6 +63,8 @@ int upload(T **dst, const std::vector<T> &src)
 void free_device(qsg_graph *g)
 {
     cudaFree(g->d_cn_tab); cudaFree(g->d_cn_tab_x);
+    for (auto &q : g->queues) cudaFree(q.second);
+    g->queues.clear();
     cudaFree(g->d_vn_sym); cudaFree(g->d_vn_deg); cudaFree(g->d_slot_edge);
     cudaFree(g->d_cn_ptr); cudaFree(g->d_edge_vn); cudaFree(g->d_edge_sym);
 }
@@ -367,13 +369,21 @@ int launch_decode(qsg_graph *g, const qsg_decoder_cfg *cfg, qsg::KParams &p, cud
     const int64_t want = (p.count + lc.groups - 1) / lc.groups;
     const int grid = (int)std::min<int64_t>(want, (int64_t)lc.ctas_per_sm * g->num_sms);
     unsigned long long *queue = nullptr;
-    QSG_CUDA(cudaMallocAsync((void **)&queue, sizeof(unsigned long long), st));
+    {
+        std::lock_guard<std::mutex> lock(g->mu);
+        auto it = g->queues.find(st);
+        if (it == g->queues.end()) {
+            QSG_CUDA(cudaMalloc((void **)&queue, sizeof(unsigned long long)));
+            g->queues.emplace(st, queue);
+        } else {
+            queue = it->second;
+        }
+    }
     QSG_CUDA(cudaMemsetAsync(queue, 0, sizeof(unsigned long long), st));
     p.queue = queue;
     p.groups = lc.groups;
     void *args[] = {&p};
     cudaError_t err = cudaLaunchKernel(fn, dim3(grid), dim3(lc.groups * g->threads), args, lc.smem, st);
-    cudaFreeAsync(queue, st);
     if (err != cudaSuccess) return fail(QSG_ECUDA, std::string("decode launch: ") + cudaGetErrorString(err));
     return QSG_OK;
 }

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -60,4 +61,10 @@ struct qsg_graph {
     // launch configurations cached per kernel instance
     std::mutex mu;
     qsg::LaunchCfg cfg_cache[2][2];  // [bp4][additive]
+    // frame-queue counter per stream: launches on one stream are ordered, so
+    // one 8-byte counter (re-zeroed before each launch) serves them all; no
+    // per-launch allocation (the stream-ordered pool returns freed memory at
+    // every synchronisation, making a per-launch cudaMallocAsync cost
+    // ~200 us after each sync)
+    std::unordered_map<cudaStream_t, unsigned long long *> queues;
 };
