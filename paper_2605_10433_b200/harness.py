@@ -187,6 +187,54 @@ def config_digest(cfg: SweepConfig) -> str:
     return hashlib.sha256(canonical_json(_config_dict(cfg)).encode()).hexdigest()
 
 
+#: Optional FER unit with the ``_decode_frames`` signature used by
+#: run_point / run_sweep instead of the device pipeline (e.g. the CPU oracle
+#: in the protocol tests).  None: the GPU.
+FRAME_UNIT = None
+
+
+def frame_batches(graph, decoder_cfg, epsilon, epsilon0, seed, stop, batch_frames):
+    """Yield (fails, iterations) numpy arrays for frames [0, stop) in order,
+    batch by batch, keeping the next batch's launch queued on the device
+    while the current one is handed back (speculative, like the reference's
+    worker pool: a consumer that stops early discards it, harness.py:200-246).
+    Two persistent pinned staging buffers; one event per batch."""
+    if FRAME_UNIT is not None:
+        for start in range(0, stop, batch_frames):
+            yield FRAME_UNIT(graph, decoder_cfg, epsilon, epsilon0, seed, start, min(batch_frames, stop - start))
+        return
+    dg = device_graph(graph)
+    n = min(batch_frames, stop)
+    stages = [torch.empty(9 * n, dtype=torch.uint8, pin_memory=True) for _ in range(2)] if n else []
+    inflight = []
+
+    def launch(start, k):
+        count = min(batch_frames, stop - start)
+        fails, iters, _ = decode_frames_device(dg, decoder_cfg, epsilon, epsilon0, seed, start, count)
+        st = stages[k % 2]
+        st[: 8 * count].view(torch.int64).copy_(iters, non_blocking=True)
+        st[8 * count: 9 * count].copy_(fails, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(dg.device))
+        inflight.append((ev, st, count))
+
+    starts = list(range(0, stop, batch_frames))
+    try:
+        for k, start in enumerate(starts[:2]):
+            launch(start, k)
+        for k in range(len(starts)):
+            ev, st, count = inflight.pop(0)
+            ev.synchronize()
+            fails = st[8 * count: 9 * count].numpy().astype(bool)
+            iters = st[: 8 * count].view(torch.int64).numpy().copy()
+            if k + 2 < len(starts):
+                launch(starts[k + 2], k + 2)  # reuses this batch's staging buffer (already copied out)
+            yield fails, iters
+    finally:  # a consumer that stopped early: let the speculative copies land before the buffers go
+        for ev, _, _ in inflight:
+            ev.synchronize()
+
+
 def run_point(graph, cfg: SweepConfig, epsilon: float, batch_frames: int = GPU_BATCH_FRAMES) -> FerPoint:
     """FER at one noise level under the ordered stop rule (harness.py:248-293):
     stop at the smallest frame index where cumulative failures reach the
@@ -195,9 +243,9 @@ def run_point(graph, cfg: SweepConfig, epsilon: float, batch_frames: int = GPU_B
     digest = config_digest(cfg)
     frames = failures = iter_sum = 0
     start = 0
-    while start < cfg.max_frames:
-        count = min(batch_frames, cfg.max_frames - start)
-        fails, iters = decode_frames(graph, cfg.decoder, epsilon, eps0, cfg.seed, start, count)
+    batches = frame_batches(graph, cfg.decoder, epsilon, eps0, cfg.seed, cfg.max_frames, batch_frames)
+    for fails, iters in batches:
+        count = len(fails)
         cum = np.cumsum(fails)
         hit = np.nonzero(failures + cum >= cfg.target_failures)[0]
         if hit.size:
@@ -210,6 +258,7 @@ def run_point(graph, cfg: SweepConfig, epsilon: float, batch_frames: int = GPU_B
         failures += int(cum[-1]) if count else 0
         iter_sum += int(iters.sum())
         start += count
+    batches.close()
     low, high = wilson_interval(failures, frames)
     point = FerPoint(epsilon=epsilon, epsilon0=eps0, frames=frames, failures=failures,
                      fer=failures / frames, wilson_low=low, wilson_high=high,

@@ -89,11 +89,12 @@ def test_digest_equals_reference(reference):
 
 @pytest.fixture
 def cpu_fer_unit(monkeypatch, oracle):
-    """Route harness.decode_frames to the oracle (protocol test on CPU)."""
+    """Run the FER protocol on the oracle (harness.FRAME_UNIT hook; protocol
+    test on CPU)."""
     def unit(graph, cfg, eps, eps0, seed, start, count):
         f, it, _, _ = oracle.frames(oracle.Graph(graph), cfg, eps, eps0, seed, start, count, precision=64)
         return f, it
-    monkeypatch.setattr(H, "decode_frames", unit)
+    monkeypatch.setattr(H, "FRAME_UNIT", unit)
 
 
 @pytest.mark.parametrize("batch", [1 << 20, 7, 4096])
