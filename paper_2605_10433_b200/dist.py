@@ -9,11 +9,11 @@ bit-identical per-frame results (reference harness.py:1-11).  Two modes:
     (NCCL over NVLink; latency-bound, ~32 bytes).
   * ``run_point_sharded``: the reference's ordered stop rule
     (harness.py:262-270) across ranks.  Frames are processed in rounds of
-    world x chunk; each rank decodes its contiguous sub-range and the
-    per-frame fail flags and iteration counts are all-gathered in frame order
-    so every rank applies the same cumulative-failure stop rule; frames past
-    the stop index are discarded as the reference does for speculative
-    batches.
+    world x chunk; each rank decodes its contiguous sub-range, the ranks
+    all-gather their (failures, sum iterations) scalars, and only the rank
+    whose prefix crosses the target searches its own fail flags (on its
+    device) for the stop frame and broadcasts it; frames past the stop index
+    are discarded as the reference does for speculative batches.
 
 The per-rank FER unit is pluggable (``unit``) so the host logic is testable
 with the gloo backend on CPU; the product path uses ``decode_frames_device``
@@ -76,7 +76,14 @@ class ShardedStats:
 def run_point_sharded(graph, cfg: SweepConfig, epsilon: float, *, chunk: int = 1 << 20, unit=None,
                       device=None) -> FerPoint:
     """run_point (harness.py:248-293) with frames sharded over all ranks and
-    the exact ordered stop rule; every rank returns the same FerPoint."""
+    the exact ordered stop rule; every rank returns the same FerPoint.
+
+    Per round of world x chunk frames only scalars cross ranks: ONE
+    all-gather of each rank's (failures, sum iterations).  If the global
+    cumulative count reaches the target inside the round, the first rank
+    whose prefix crosses it finds its local stop frame and iteration prefix
+    on its own device and broadcasts those two numbers -- frames past the
+    stop are discarded, as the reference does for speculative batches."""
     rank, world = _world()
     unit = unit or (lambda *a: gpu_unit(*a, device=device))
     eps0 = epsilon if cfg.epsilon0_mode == "matched" else float(cfg.epsilon0)
@@ -86,34 +93,46 @@ def run_point_sharded(graph, cfg: SweepConfig, epsilon: float, *, chunk: int = 1
         count = min(chunk * world, cfg.max_frames - start)
         lo, n = shard_range(rank, world, start, count)
         fails, iters = unit(graph, cfg.decoder, epsilon, eps0, cfg.seed, lo, n)
-        fails = fails.to(torch.int32)
-        iters = iters.to(torch.int32)
+        fails = fails.to(torch.int64)
+        iters = iters.to(torch.int64)
+        mine = torch.stack([fails.sum(), iters.sum()]) if n else torch.zeros(2, dtype=torch.int64,
+                                                                             device=fails.device)
         if world > 1:
-            sizes = [shard_range(r, world, start, count)[1] for r in range(world)]
-            pad = max(sizes)
-            fpad = torch.zeros(pad, dtype=torch.int32, device=fails.device)
-            ipad = torch.zeros(pad, dtype=torch.int32, device=iters.device)
-            fpad[:n] = fails
-            ipad[:n] = iters
-            fl = [torch.empty_like(fpad) for _ in range(world)]
-            il = [torch.empty_like(ipad) for _ in range(world)]
-            dist.all_gather(fl, fpad)
-            dist.all_gather(il, ipad)
-            fails = torch.cat([t[:s] for t, s in zip(fl, sizes)])
-            iters = torch.cat([t[:s] for t, s in zip(il, sizes)])
-        f64 = fails.to(torch.int64).cpu()
-        cum = torch.cumsum(f64, 0)
-        hit = torch.nonzero(failures + cum >= cfg.target_failures)
-        if hit.numel():
-            stop = int(hit[0, 0]) + 1
-            frames = start + stop
-            failures += int(cum[stop - 1])
-            iter_sum += int(iters[:stop].to(torch.int64).sum())
-            break
-        frames = start + count
-        failures += int(cum[-1]) if count else 0
-        iter_sum += int(iters.to(torch.int64).sum())
-        start += count
+            allv = [torch.empty_like(mine) for _ in range(world)]
+            dist.all_gather(allv, mine)
+            per = torch.stack(allv).cpu().tolist()
+        else:
+            per = [mine.cpu().tolist()]
+        before = failures
+        crossing = None
+        for r, (nf, _) in enumerate(per):
+            if before + nf >= cfg.target_failures:
+                crossing = r
+                break
+            before += nf
+        if crossing is None:
+            frames = start + count
+            failures = before
+            iter_sum += sum(ni for _, ni in per)
+            start += count
+            continue
+        # the crossing rank locates the stop frame inside its shard
+        if rank == crossing:
+            cum = torch.cumsum(fails, 0)
+            k = int(torch.nonzero(before + cum >= cfg.target_failures)[0, 0])
+            info = torch.tensor([k, int(iters[: k + 1].sum())], dtype=torch.int64, device=mine.device)
+        else:
+            info = torch.zeros(2, dtype=torch.int64, device=mine.device)
+        if world > 1:
+            dist.broadcast(info, src=crossing)
+        k, it_prefix = (int(x) for x in info.cpu().tolist())
+        lo_c, _ = shard_range(crossing, world, start, count)
+        frames = lo_c + k + 1
+        # failures grow by at most one per frame, so the first crossing frame
+        # brings the cumulative count to exactly the target
+        failures = cfg.target_failures
+        iter_sum += sum(ni for _, ni in per[:crossing]) + it_prefix
+        break
     low, high = wilson_interval(failures, frames)
     return FerPoint(epsilon=epsilon, epsilon0=eps0, frames=frames, failures=failures,
                     fer=failures / frames, wilson_low=low, wilson_high=high,

@@ -51,7 +51,15 @@ def _worker(rank, world, port, out):
     sweep2 = P.SweepConfig(code_id="toy", decoder=P.DecoderConfig("ms", l_max=1), epsilon_list=(0.5,),
                            seed=2718, target_failures=50, max_frames=100_000)
     p2 = D.run_point_sharded(toy, sweep2, 0.5, chunk=3, unit=_oracle_unit)
-    out[rank] = {"cnt": cnt.tolist(), "p1": asdict(p1), "p2": asdict(p2)}
+    # the stop frame (index 55) in rank 1's shard: last element (chunk 4) and
+    # first element (chunk 1); and a cap-hit point (target never reached)
+    p3 = D.run_point_sharded(toy, sweep2, 0.5, chunk=4, unit=_oracle_unit)
+    p4 = D.run_point_sharded(toy, sweep2, 0.5, chunk=1, unit=_oracle_unit)
+    sweep3 = P.SweepConfig(code_id="toy", decoder=P.DecoderConfig("ms", l_max=1), epsilon_list=(0.5,),
+                           seed=2718, target_failures=50, max_frames=41)
+    p5 = D.run_point_sharded(toy, sweep3, 0.5, chunk=7, unit=_oracle_unit)
+    out[rank] = {"cnt": cnt.tolist(), "p1": asdict(p1), "p2": asdict(p2), "p3": asdict(p3), "p4": asdict(p4),
+                 "p5": asdict(p5)}
     dist.destroy_process_group()
 
 
@@ -70,7 +78,18 @@ def test_two_rank_gloo(oracle):
     for r in range(world):
         assert out[r]["cnt"] == c.tolist()
     gold = json.loads((GOLD / "golden_harness.json").read_text())
+    from paper_2605_10433_b200 import harness as H
+    H.FRAME_UNIT = lambda *a: tuple(x.numpy() for x in _oracle_unit(*a))
+    try:
+        toy = P.gb_graph(P.GbSpec(*TOY))
+        capped = H.run_point(toy, P.SweepConfig(code_id="toy", decoder=P.DecoderConfig("ms", l_max=1),
+                                                epsilon_list=(0.5,), seed=2718, target_failures=50,
+                                                max_frames=41), 0.5)
+    finally:
+        H.FRAME_UNIT = None
     for r in range(world):
         assert out[r]["p1"] == gold["small_sagms_eps025"]["point"]
         assert out[r]["p2"] == gold["toy_ms_lmax1_eps05"]["point"]
+        assert out[r]["p3"] == out[r]["p4"] == gold["toy_ms_lmax1_eps05"]["point"]
+        assert out[r]["p5"] == asdict(capped) and capped.cap_hit and capped.frames == 41
     assert P.dist.shard_range(0, 3, 10, 8) == (10, 2) and P.dist.shard_range(2, 3, 10, 8) == (15, 3)

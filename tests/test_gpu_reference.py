@@ -190,3 +190,22 @@ def test_degenerate_equivalences_bit_identical(P):
         tb = P.decode(None, g, syn[0], prior, b, capture_messages=True, early_stop=False)
         for sa, sb in zip(ta.message_trace, tb.message_trace):
             assert np.array_equal(sa.vn_to_cn, sb.vn_to_cn) and np.array_equal(sa.cn_to_vn, sb.cn_to_vn)
+
+
+def test_sharded_point_on_device_matches_reference(P):
+    """dist.run_point_sharded with the device FER unit (world size 1 here;
+    the multi-rank exchange is covered on CPU by tests/test_dist.py) and
+    dist.fer_counters give the reference's FerPoint / counts."""
+    from paper_2605_10433_b200 import dist as D
+    gold = json.loads((GOLD / "golden_harness.json").read_text())
+    small = P.gb_graph(P.GbSpec(*SMALL))
+    g = P.GainParams(0.3, 0.5, 1.1)
+    sweep = P.SweepConfig(code_id="gb-10-2", decoder=P.DecoderConfig("sagms", l_max=4, gain=g),
+                          epsilon_list=(0.25,), seed=31, target_failures=40, max_frames=100_000)
+    for chunk in (5, 1 << 20):
+        pt = D.run_point_sharded(small, sweep, 0.25, chunk=chunk)
+        assert asdict(pt) == gold["small_sagms_eps025"]["point"]
+    cfg = P.DecoderConfig("sagms", l_max=8, gain=g)
+    cnt = D.fer_counters(small, cfg, 0.2, 0.2, 7, 3, 1001)
+    fails, iters = P.decode_frames(small, cfg, 0.2, 0.2, 7, 3, 1001)
+    assert cnt.cpu().tolist() == [1001, int(fails.sum()), int(iters.sum()), small.edge_count * (int(iters.sum()) - 1001)]
