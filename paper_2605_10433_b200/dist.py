@@ -87,9 +87,10 @@ def run_point_sharded(graph, cfg: SweepConfig, epsilon: float, *, chunk: int = 1
     rank, world = _world()
     unit = unit or (lambda *a: gpu_unit(*a, device=device))
     eps0 = epsilon if cfg.epsilon0_mode == "matched" else float(cfg.epsilon0)
-    frames = failures = iter_sum = 0
-    start = 0
-    while start < cfg.max_frames:
+
+    def launch(start):
+        """Decode this rank's shard of the round at ``start`` and queue the
+        scalar all-gather (both stream-ordered, no host sync)."""
         count = min(chunk * world, cfg.max_frames - start)
         lo, n = shard_range(rank, world, start, count)
         fails, iters = unit(graph, cfg.decoder, epsilon, eps0, cfg.seed, lo, n)
@@ -97,12 +98,19 @@ def run_point_sharded(graph, cfg: SweepConfig, epsilon: float, *, chunk: int = 1
         iters = iters.to(torch.int64)
         mine = torch.stack([fails.sum(), iters.sum()]) if n else torch.zeros(2, dtype=torch.int64,
                                                                              device=fails.device)
+        allv = [mine]
         if world > 1:
             allv = [torch.empty_like(mine) for _ in range(world)]
             dist.all_gather(allv, mine)
-            per = torch.stack(allv).cpu().tolist()
-        else:
-            per = [mine.cpu().tolist()]
+        return start, count, fails, iters, mine, allv
+
+    frames = failures = iter_sum = 0
+    nxt = launch(0) if cfg.max_frames > 0 else None
+    while nxt is not None:
+        start, count, fails, iters, mine, allv = nxt
+        # speculative: the next round is queued before this one is inspected
+        nxt = launch(start + count) if start + count < cfg.max_frames else None
+        per = torch.stack(allv).cpu().tolist()
         before = failures
         crossing = None
         for r, (nf, _) in enumerate(per):
@@ -114,7 +122,6 @@ def run_point_sharded(graph, cfg: SweepConfig, epsilon: float, *, chunk: int = 1
             frames = start + count
             failures = before
             iter_sum += sum(ni for _, ni in per)
-            start += count
             continue
         # the crossing rank locates the stop frame inside its shard
         if rank == crossing:
