@@ -587,12 +587,13 @@ __device__ __forceinline__ void cn_update_fixed(const uint16_t *row, uint32_t ms
     }
 }
 
-// Inline both circulant halves (check c and l + c, qubit c and l + c) only
-// where the extra code still fits the instruction cache: the min-sum
-// kernels with one warp per frame.  BP4 (20 inlined phi per check) and the
-// 128-thread kernels measured faster with a single copy in a loop.
+// Inline both circulant halves (check c and l + c, qubit c and l + c) in the
+// min-sum kernels (more independent work per lane; +4-5% on the 128-thread
+// kernels once the paired math made the qubit update short).  BP4 (20
+// inlined phi per check) keeps one copy in a loop: unrolled it overflows
+// the instruction cache (-25% measured).
 template <int T, bool BP4>
-constexpr bool kUnrollPair = T == 32 && !BP4;
+constexpr bool kUnrollPair = !BP4;
 
 template <int W, int T, bool BP4>
 __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, uint32_t syn_bits,
