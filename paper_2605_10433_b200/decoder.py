@@ -147,6 +147,46 @@ def decode_batch_device(graph, syndromes: torch.Tensor, l0: float, cfg, *, early
     return out
 
 
+_STAGE: dict = {}
+
+
+def _stage(key, nbytes: int) -> torch.Tensor:
+    """Grow-only pinned host staging buffer per (thread, device, role)."""
+    import threading
+    k = (threading.get_ident(), torch.cuda.current_device(), key)
+    buf = _STAGE.get(k)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, pin_memory=True)
+        _STAGE[k] = buf
+    return buf
+
+
+def _pinned_from(a: np.ndarray) -> torch.Tensor:
+    """A numpy array staged in pinned memory (for an asynchronous H2D copy);
+    valid until the next call on this thread."""
+    a = np.ascontiguousarray(a)
+    buf = _stage("in", a.nbytes)[: a.nbytes]
+    np.copyto(buf.numpy().view(a.dtype).reshape(a.shape), a)
+    return buf.view(torch.from_numpy(a[:0].reshape(-1)).dtype).view(a.shape)
+
+
+def _to_host(tensors: dict) -> dict:
+    """Device tensors -> fresh numpy arrays through one pinned staging
+    buffer and one stream sync."""
+    total = sum((t.numel() * t.element_size() + 15) // 16 * 16 for t in tensors.values())
+    buf = _stage("out", total)
+    views, off = {}, 0
+    for k, t in tensors.items():
+        nb = t.numel() * t.element_size()
+        v = buf[off: off + nb].view(t.dtype).view(t.shape)
+        v.copy_(t, non_blocking=True)
+        views[k] = v
+        off += (nb + 15) // 16 * 16
+    if tensors:
+        torch.cuda.current_stream(next(iter(tensors.values())).device).synchronize()
+    return {k: v.numpy().copy() for k, v in views.items()}
+
+
 def decode_batch(graph, syndromes, prior: ChannelPrior, cfg, *, early_stop: bool = True,
                  collect_gamma: bool = False, capture_messages: bool = False) -> BatchDecodeResult:
     """Decode a batch of syndromes (decoder.py:374-485) on the GPU.
@@ -161,13 +201,17 @@ def decode_batch(graph, syndromes, prior: ChannelPrior, cfg, *, early_stop: bool
     if capture_messages and syn.shape[0] != 1:
         raise ValueError("capture_messages requires a single-frame batch")
     dg = device_graph(graph)
-    out = decode_batch_device(dg, torch.from_numpy(syn).to(dg.device), prior.llr, cfg,
+    # pinned staging both ways (torch caches pinned blocks) and one sync:
+    # pageable copies of B x m and B x n bytes cost ~4x more than the decode
+    d_syn = _pinned_from(syn).to(dg.device, non_blocking=True)
+    out = decode_batch_device(dg, d_syn, prior.llr, cfg,
                               early_stop=early_stop, collect_gamma=collect_gamma,
                               capture_messages=capture_messages)
+    host = _to_host({k: out[k] for k in ("success", "e_hat", "iterations")})
     res = BatchDecodeResult(
-        success=out["success"].cpu().numpy().astype(bool),
-        e_hat=out["e_hat"].cpu().numpy(),
-        iterations=out["iterations"].cpu().numpy(),
+        success=host["success"].astype(bool),
+        e_hat=host["e_hat"],
+        iterations=host["iterations"],
     )
     if collect_gamma or capture_messages:
         unsat = out["unsat"].cpu().numpy()
@@ -216,9 +260,11 @@ def decode_batch_packed(graph, syn_words, prior: ChannelPrior, cfg) -> BatchDeco
     """decode_batch for bit-packed syndromes (see pack_syndromes)."""
     dg = device_graph(graph)
     w = np.ascontiguousarray(syn_words, dtype=np.uint32).view(np.int32)
-    out = decode_batch_packed_device(dg, torch.from_numpy(w).to(dg.device), prior.llr, cfg, e_hat=True)
-    return BatchDecodeResult(success=out["success"].cpu().numpy().astype(bool),
-                             e_hat=out["e_hat"].cpu().numpy(), iterations=out["iterations"].cpu().numpy())
+    out = decode_batch_packed_device(dg, _pinned_from(w).to(dg.device, non_blocking=True), prior.llr, cfg,
+                                     e_hat=True)
+    host = _to_host({k: out[k] for k in ("success", "e_hat", "iterations")})
+    return BatchDecodeResult(success=host["success"].astype(bool), e_hat=host["e_hat"],
+                             iterations=host["iterations"])
 
 
 def decode(H, graph, s, prior: ChannelPrior, cfg, *, early_stop: bool = True,
