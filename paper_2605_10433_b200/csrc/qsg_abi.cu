@@ -360,7 +360,8 @@ int launch_decode(qsg_graph *g, const qsg_decoder_cfg *cfg, qsg::KParams &p, cud
 {
     const bool bp4 = cfg->variant == QSG_BP4, add = cfg->vn_mode == QSG_VN_ADDITIVE;
     if (!bp4 && g->d_cn_tab_x) p.cn_tab = g->d_cn_tab_x;
-    void *fn = qsg::kernel_ptr(g->kind, g->threads, bp4, add, g->n_pad);
+    void *fn = qsg::kernel_ptr(g->kind, g->threads, bp4, add,
+                               g->kind > 0 ? g->n_pad : std::max(g->dc_max, g->dv_max));
     if (!fn) return fail(QSG_EUNSUPPORTED, "no kernel for this graph kind");
     qsg::LaunchCfg lc;
     int rc = launch_cfg(g, bp4, add, fn, &lc);

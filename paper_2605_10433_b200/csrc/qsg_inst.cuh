@@ -15,19 +15,27 @@ static void *pick(bool bp4, bool add)
     return add ? (void *)decode_kernel<QSG_W, T, false, true, NP> : (void *)decode_kernel<QSG_W, T, false, false, NP>;
 }
 
-// np: compile-time qubit stride for the bicycle one-warp kernels at n_pad =
-// 256 (every l in (64, 128], the BASELINE codes); 0 = run-time stride.
+// np: bicycle kernels (W > 0): compile-time qubit stride n_pad (0 = run
+// time); generic kernels (W == 0): the node-degree bound (8, 12, 16, 24 or
+// 32) that sizes their register arrays.
 void *QSG_FN(QSG_W)(int T, bool bp4, bool add, int np)
 {
-#if QSG_W > 0
+#if QSG_W == 0
+    if (T != 32 && T != 128) return nullptr;
+    if (np <= 8) return T == 32 ? pick<32, 8>(bp4, add) : pick<128, 8>(bp4, add);
+    if (np <= 12) return T == 32 ? pick<32, 12>(bp4, add) : pick<128, 12>(bp4, add);
+    if (np <= 16) return T == 32 ? pick<32, 16>(bp4, add) : pick<128, 16>(bp4, add);
+    if (np <= 24) return T == 32 ? pick<32, 24>(bp4, add) : pick<128, 24>(bp4, add);
+    return T == 32 ? pick<32, 32>(bp4, add) : pick<128, 32>(bp4, add);
+#else
     if (T == 32 && np == 256) return pick<32, 256>(bp4, add);
     if (T == 32 && np == 128) return pick<32, 128>(bp4, add);
     if (T == 128 && np == 512) return pick<128, 512>(bp4, add);
     if (T == 128 && np == 1024) return pick<128, 1024>(bp4, add);
-#endif
     if (T == 32) return pick<32, 0>(bp4, add);
     if (T == 128) return pick<128, 0>(bp4, add);
     return nullptr;
+#endif
 }
 
 }  // namespace qsg

@@ -164,6 +164,37 @@ __device__ __forceinline__ float pairwise_rt(const float *a, int n)
 }
 __device__ __forceinline__ float segsum_rt(const float *a, int n) { return a[0] + pairwise_rt(a + 1, n - 1); }
 
+// segsum_rt for a run-time length d <= DM with every index compile-time (the
+// generic kernels keep their per-node arrays in registers): the same numpy
+// tree -- x0 + pairwise(x1..x_{d-1}), sequential below 8 elements, else 8
+// strided accumulators, their tree and a sequential tail -- with the unused
+// steps predicated off (adding -0.0 is an exact no-op).
+template <int DM>
+__device__ __forceinline__ float segsum_pred(const float (&x)[DM], int d)
+{
+    const int n = d - 1;  // length of the pairwise part x[1..d-1]
+    float res = -0.0f;
+    if (DM <= 8 || n < 8) {
+#pragma unroll
+        for (int k = 1; k < (DM < 8 ? DM : 8); ++k) res = res + (k <= n ? x[k] : -0.0f);
+    } else {
+        if constexpr (DM > 8) {
+            float r[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) r[k] = x[1 + k];
+            const int lim = n - (n % 8);
+#pragma unroll
+            for (int i = 8; i + 8 <= DM - 1; i += 8)
+#pragma unroll
+                for (int k = 0; k < 8; ++k) r[k] = r[k] + (i < lim ? x[1 + i + k] : -0.0f);
+            res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+#pragma unroll
+            for (int i = 8; i < DM - 1; ++i) res = res + ((i >= lim && i < n) ? x[1 + i] : -0.0f);
+        }
+    }
+    return x[0] + res;
+}
+
 // argmin over (0, mX, mZ, mY) with ties to the lowest code (np.argmin,
 // decoder.py:301).
 __device__ __forceinline__ uint32_t hard_decision(float mX, float mZ, float mY)
@@ -281,7 +312,7 @@ __device__ __forceinline__ void sts_u(unsigned char *base, uint32_t off, uint32_
 
 // ---- generic residual (table-driven, decoder.py:303-309) -------------------
 // Bits of this thread's checks; bit t <-> check tid + t*T.
-template <int T>
+template <int T, int DM>
 __device__ __forceinline__ uint32_t syndrome_bits_generic(const KParams &p, const GroupMem &gm, int tid)
 {
     uint32_t bits = 0;
@@ -293,11 +324,14 @@ __device__ __forceinline__ uint32_t syndrome_bits_generic(const KParams &p, cons
         const uint32_t *row = gm.tab + i * p.row_words;
         uint32_t x = 0;
         const int d = (int)row[p.dc_max];
-        for (int k = 0; k < d; ++k) {
-            const uint32_t ent = row[k];
-            const uint32_t c = *reinterpret_cast<const uint32_t *>(eb + (ent & jmask));
-            const uint32_t sym = ent >> 30;
-            x ^= ((c & 1u) & (sym >> 1)) ^ ((c >> 1) & (sym & 1u));
+#pragma unroll
+        for (int k = 0; k < DM; ++k) {
+            if (k < d) {
+                const uint32_t ent = row[k];
+                const uint32_t c = *reinterpret_cast<const uint32_t *>(eb + (ent & jmask));
+                const uint32_t sym = ent >> 30;
+                x ^= ((c & 1u) & (sym >> 1)) ^ ((c >> 1) & (sym & 1u));
+            }
         }
         bits |= (x & 1u) << t;
     }
@@ -595,7 +629,7 @@ __device__ __forceinline__ void cn_update_fixed(const uint16_t *row, uint32_t ms
 template <int T, bool BP4>
 constexpr bool kUnrollPair = !BP4;
 
-template <int W, int T, bool BP4>
+template <int W, int T, bool BP4, int NP>
 __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, uint32_t syn_bits,
                                          uint32_t res_bits, float g0, float g1, int tid)
 {
@@ -623,6 +657,8 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, u
         }
     } else {
         constexpr uint32_t kAddr = 0x00ffffffu;  // generic entries carry sym << 30
+        constexpr int DM = NP > 0 ? NP : kGenericMaxDeg;  // degree bound of this instantiation
+        const uint32_t msg_s = smem_addr(msg);
         int t = 0;
 #pragma unroll 1
         for (int i = tid; i < p.m; i += T, ++t) {
@@ -630,39 +666,49 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, u
             const uint32_t sneg = ((syn_bits >> t) & 1u) << 31;
             const float gain = ((res_bits >> t) & 1u) ? g1 : g0;
             const int d = (int)row[p.dc_max];
-            uint32_t off[kGenericMaxDeg];
-            float v[kGenericMaxDeg];
+            uint32_t ad[DM];
+            float v[DM];
             uint32_t sx = sneg;
-            for (int k = 0; k < d; ++k) {
-                off[k] = row[k] & kAddr;
-                v[k] = lds_f(msg, off[k]);
-                sx ^= f2u(v[k]);
+#pragma unroll
+            for (int k = 0; k < DM; ++k) {
+                ad[k] = msg_s + (k < d ? (row[k] & kAddr) : 0u);
+                v[k] = k < d ? lds_a(ad[k]) : __int_as_float(0x7f800000);  // +inf: neutral for min
+                sx ^= k < d ? f2u(v[k]) : 0u;
             }
             const uint32_t sgn = sx & 0x80000000u;
             if constexpr (BP4) {
-                float ph[kGenericMaxDeg];
-                for (int k = 0; k < d; ++k) ph[k] = phi(fmaxf(fminf(fabsf(v[k]), kClip), 1e-12f));
-                const float total = segsum_rt(ph, d);
-                for (int k = 0; k < d; ++k) {
-                    const float ext = fminf(fmaxf(total - ph[k], 1e-12f), 50.0f);
-                    const uint32_t mag = f2u(fminf(phi(ext), kClip)) ^ sgn;
-                    sts_u(msg, off[k], (f2u(v[k]) & 0x80000000u) ^ mag);
+                float ph[DM], r[DM];
+#pragma unroll
+                for (int k = 0; k < DM; k += 2) {
+                    const F2 y = phi2(pk(fmaxf(fminf(fabsf(v[k]), kClip), 1e-12f),
+                                         fmaxf(fminf(fabsf(v[k + 1]), kClip), 1e-12f)));
+                    ph[k] = lo(y); ph[k + 1] = hi(y);
                 }
+                const float total = segsum_pred<DM>(ph, d);
+#pragma unroll
+                for (int k = 0; k < DM; k += 2) {
+                    const F2 e = sub2(bc(total), pk(ph[k], ph[k + 1]));
+                    const F2 y = phi2(pk(fminf(fmaxf(lo(e), 1e-12f), 50.0f), fminf(fmaxf(hi(e), 1e-12f), 50.0f)));
+                    r[k] = lo(y); r[k + 1] = hi(y);
+                }
+#pragma unroll
+                for (int k = 0; k < DM; ++k)
+                    if (k < d) sts_a(ad[k], (f2u(v[k]) & 0x80000000u) ^ f2u(fminf(r[k], kClip)) ^ sgn);
             } else {
                 float mn1 = __int_as_float(0x7f800000), mn2 = mn1;
-                for (int k = 0; k < d; ++k) {
+#pragma unroll
+                for (int k = 0; k < DM; ++k) {
                     const float a = fabsf(v[k]);
                     mn2 = fminf(mn2, fmaxf(mn1, a));
                     mn1 = fminf(mn1, a);
                 }
                 mn1 = fminf(mn1, kClip);
                 mn2 = fminf(mn2, kClip);
-                const uint32_t m1 = f2u(fminf(gain * mn1, kClip)) ^ sgn;
-                const uint32_t m2 = f2u(fminf(gain * mn2, kClip)) ^ sgn;
-                for (int k = 0; k < d; ++k) {
-                    const uint32_t mag = fabsf(v[k]) == mn1 ? m2 : m1;
-                    sts_u(msg, off[k], (f2u(v[k]) & 0x80000000u) ^ mag);
-                }
+                const uint32_t m1 = xor_pin(f2u(fminf(gain * mn1, kClip)), sgn);
+                const uint32_t m2 = xor_pin(f2u(fminf(gain * mn2, kClip)), sgn);
+#pragma unroll
+                for (int k = 0; k < DM; ++k)
+                    if (k < d) sts_a(ad[k], sign_merge(f2u(v[k]), fabsf(v[k]) == mn1 ? m2 : m1));
             }
         }
     }
@@ -750,40 +796,45 @@ __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, i
             }
         }
     } else {
+        constexpr int DM = NP > 0 ? NP : kGenericMaxDeg;  // degree bound of this instantiation
+        const F2 kapc2 = bc(kapc);
 #pragma unroll 1
         for (int j = tid; j < p.n; j += T) {
-            unsigned char *col = msg + 4 * j;
+            const uint32_t cs = smem_addr(msg + 4 * j);
             const int d = gm.vn_deg[j];
-            float c[kGenericMaxDeg], tmp[kGenericMaxDeg];
-            uint32_t sym[kGenericMaxDeg];
-            for (int s = 0; s < d; ++s) {
-                c[s] = lds_f(col, s * rowb);
-                sym[s] = gm.vn_sym[s * p.n_pad + j];
+            float c[DM], tmp[DM];
+            uint32_t sym[DM];
+            uint32_t any_y = 0;
+#pragma unroll
+            for (int s = 0; s < DM; ++s) {
+                c[s] = s < d ? lds_a(cs + s * rowb) : 0.0f;
+                sym[s] = s < d ? gm.vn_sym[s * p.n_pad + j] : 0u;
+                any_y |= sym[s] == 3;
             }
             float b[4], tot[4];
 #pragma unroll
             for (int e = 1; e <= 3; ++e) {
-                for (int s = 0; s < d; ++s) {
+#pragma unroll
+                for (int s = 0; s < DM; ++s) {
                     const uint32_t sx = sym[s] & 1u, sz = sym[s] >> 1;
                     const uint32_t a = e == 1 ? sz : (e == 2 ? sx : (sx ^ sz));
                     tmp[s] = a ? c[s] : 0.0f;
                 }
-                tot[e] = segsum_rt(tmp, d);
+                tot[e] = segsum_pred<DM>(tmp, d);
                 b[e] = l0 + tot[e];
             }
-            const float sumz = tot[1], sumx = tot[2];
             gm.ehat[j] = hard_decision(b[1], b[2], b[3]);
             if constexpr (ADD) {
-                for (int s = 0; s < d; ++s) tmp[s] = c[s];
-                const float all = segsum_rt(tmp, d);
-                for (int s = 0; s < d; ++s) sts_u(col, s * rowb, f2u(l0 + (all - c[s])));
+                const float all = segsum_pred<DM>(c, d);
+#pragma unroll
+                for (int s = 0; s < DM; ++s)
+                    if (s < d) sts_a(cs + s * rowb, f2u(l0 + (all - c[s])));  // clipped by the consumer
             } else {
                 float V[4];
-                uint32_t any_y = 0;
-                for (int s = 0; s < d; ++s) any_y |= sym[s] == 3;
                 if (!any_y) {  // b[1] - l0 = S_Z, b[2] - l0 = S_X exactly as summed
-                    V[1] = b[2] + vn_F(sumz, kapc);
-                    V[2] = b[1] + vn_F(sumx, kapc);
+                    const F2 v2 = add2(pk(b[2], b[1]), vn_F2(tot[1], tot[2], kapc2));
+                    V[1] = lo(v2);
+                    V[2] = hi(v2);
                     V[3] = 0.0f;
                 } else {
 #pragma unroll
@@ -792,7 +843,11 @@ __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, i
                         V[S] = logaddexp(0.0f, -b[S]) - logaddexp(-b[a1], -b[a2]);
                     }
                 }
-                for (int s = 0; s < d; ++s) sts_u(col, s * rowb, f2u(V[sym[s]] - c[s]));
+#pragma unroll
+                for (int s = 0; s < DM; ++s) {
+                    const float vs = sym[s] == 1 ? V[1] : (sym[s] == 2 ? V[2] : V[3]);
+                    if (s < d) sts_a(cs + s * rowb, f2u(vs - c[s]));  // clipped by the consumer
+                }
             }
         }
     }
@@ -958,7 +1013,7 @@ __global__ void __launch_bounds__(640) decode_kernel(const KParams p)
                         if (4 * b + q < n) gm.ehat[4 * b + q] = pauli_from_word(w.v[q], p.kx, p.ky, p.kz);
                 }
                 group_sync<T>(g);
-                syn_bits = syndrome_bits_generic<T>(p, gm, tid);
+                syn_bits = syndrome_bits_generic<T, (NP > 0 ? NP : kGenericMaxDeg)>(p, gm, tid);
                 group_sync<T>(g);
             } else if (p.syn_words) {
                 int t = 0;
@@ -983,7 +1038,7 @@ __global__ void __launch_bounds__(640) decode_kernel(const KParams p)
                 part = use_plan ? circ_syndrome_plan<W, T>(plan, gm, gm.synw, gm.resw, p.lpw)
                                 : circ_syndrome<W, T>(p, gm, gm.synw, gm.resw, tid);
             } else {
-                res = syn_bits ^ syndrome_bits_generic<T>(p, gm, tid);
+                res = syn_bits ^ syndrome_bits_generic<T, (NP > 0 ? NP : kGenericMaxDeg)>(p, gm, tid);
                 part = __popc(res);
             }
             const int unsat = group_sum<T>(part, scratch, ell & 1, tid, g);
@@ -1012,7 +1067,7 @@ __global__ void __launch_bounds__(640) decode_kernel(const KParams p)
                 g0 = (float)(base * 1.0);
                 g1 = (float)(base * p.eta);
             }
-            cn_phase<W, T, BP4>(p, gm, syn_bits, res, g0, g1, tid);
+            cn_phase<W, T, BP4, NP>(p, gm, syn_bits, res, g0, g1, tid);
             group_sync<T>(g);
             if (capture && p.tr_cn) snapshot<T>(p, gm.msg, p.tr_cn + (f * p.l_max + n_snap) * p.E, tid, false);
             vn_phase<W, T, BP4, ADD, NP>(p, gm, tid);

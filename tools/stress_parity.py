@@ -19,12 +19,33 @@ for i in range(cases):
     w = int(rng.choice([2, 3, 4, 5, 6, 8]))
     if w >= ell // 2:
         continue
-    try:
-        spec = P.random_gb_spec(ell, w, seed=int(rng.integers(1 << 30)))
-    except Exception as exc:  # no k > 0 code found quickly
-        print("skip", ell, w, exc)
-        continue
-    g = P.gb_graph(spec)
+    if rng.random() < 0.35:
+        # generic kernels: |a| != |b| GB rows, or rows with random Pauli symbols (Y-type edges)
+        wb = int(rng.integers(2, 9))
+        a = tuple(sorted(rng.choice(ell, size=w, replace=False).tolist()))
+        b = tuple(sorted(rng.choice(ell, size=wb, replace=False).tolist()))
+        if rng.random() < 0.5 or w == wb:
+            n = 2 * ell
+            rows = []
+            for i in range(int(rng.integers(ell // 2, 2 * ell))):
+                cols = sorted(rng.choice(n, size=int(rng.integers(2, 17)), replace=False).tolist())
+                rows.append([(c, int(rng.integers(1, 4))) for c in cols])
+            used = {c for r in rows for c, _ in r}
+            if len(used) < n:  # every qubit needs an edge
+                rows.append([(c, 2) for c in sorted(set(range(n)) - used)][:32])
+                used = {c for r in rows for c, _ in r}
+                if len(used) < n:
+                    continue
+            g = P.csr_graph(n, rows)
+        else:
+            g = P.gb_graph(P.GbSpec(ell, a, b))
+    else:
+        try:
+            spec = P.random_gb_spec(ell, w, seed=int(rng.integers(1 << 30)))
+        except Exception as exc:  # no k > 0 code found quickly
+            print("skip", ell, w, exc)
+            continue
+        g = P.gb_graph(spec)
     variant = str(rng.choice(["bp4", "ms", "sms", "sagms"]))
     kw = {"alpha": float(rng.choice([0.5, 0.75, 1.0]))} if variant == "sms" else {}
     if variant == "sagms":
