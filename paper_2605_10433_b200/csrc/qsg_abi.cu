@@ -416,6 +416,20 @@ void fill_cfg_params(const qsg_decoder_cfg *c, double l0, qsg::KParams &p)
     p.v0 = (float)v0;
     p.alpha = (float)c->alpha;
     p.amin = c->alpha_min; p.amax = c->alpha_max; p.eta = c->eta_unsat;
+    // SAGMS gains per unsat count (decoder.py:464-465), the kernel's double
+    // recipe evaluated here once instead of a double division per iteration
+    // and frame; volatile keeps each product rounded (no contraction)
+    p.use_gtab = (p.gain_mode == 2 && p.m < qsg::kGainTab) ? 1 : 0;
+    if (p.use_gtab) {
+        for (int u = 0; u <= p.m; ++u) {
+            const double gamma = (double)u / (double)p.m;
+            volatile double prod = (p.amax - p.amin) * gamma;
+            const double base = p.amax - prod;
+            volatile double b1 = base * 1.0, be = base * p.eta;
+            p.gtab[2 * u] = (float)b1;
+            p.gtab[2 * u + 1] = (float)be;
+        }
+    }
 }
 
 // ---- standalone sampling / syndrome kernels ----------------------------------

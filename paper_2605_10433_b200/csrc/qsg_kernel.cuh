@@ -50,6 +50,8 @@
 namespace qsg {
 
 constexpr int kGenericMaxDeg = 32;
+// SAGMS gain table: (g0, g1) per unsat count 0..m, for m < kGainTab
+constexpr int kGainTab = 1025;
 
 struct KParams {
     // graph tables (global; copied to shared memory per CTA)
@@ -68,6 +70,8 @@ struct KParams {
     float l0, v0, alpha;
     float kapc;  // e^-l0 (vn_F)
     double amin, amax, eta;
+    int32_t use_gtab;           // SAGMS: gains from gtab (host double, decoder.py:464-465) when m < kGainTab
+    float gtab[2 * kGainTab];   // gtab[2u] = (float)base(u), gtab[2u+1] = (float)(base(u) * eta), u = unsat
     // input
     int32_t sample;  // 1: sample frames on device; 0: read syndromes
     uint64_t seed;
@@ -1062,10 +1066,15 @@ __global__ void __launch_bounds__(640) decode_kernel(const KParams p)
             if (p.gain_mode == 1) {
                 g0 = g1 = p.alpha;
             } else if (p.gain_mode == 2) {
-                const double gamma = (double)unsat / (double)m;
-                const double base = p.amax - (p.amax - p.amin) * gamma;
-                g0 = (float)(base * 1.0);
-                g1 = (float)(base * p.eta);
+                if (p.use_gtab) {  // the same double recipe, tabulated per unsat count by the host
+                    g0 = p.gtab[2 * unsat];
+                    g1 = p.gtab[2 * unsat + 1];
+                } else {
+                    const double gamma = (double)unsat / (double)m;
+                    const double base = p.amax - (p.amax - p.amin) * gamma;
+                    g0 = (float)(base * 1.0);
+                    g1 = (float)(base * p.eta);
+                }
             }
             cn_phase<W, T, BP4, NP>(p, gm, syn_bits, res, g0, g1, tid);
             group_sync<T>(g);
