@@ -325,11 +325,13 @@ def run_ours(args, rank, world, local_rank):
     f_sm = (clocks["sm_mhz"] or 1965.0) * 1e6
     peak = dg_sms() * 128 * f_sm
     achieved = ops / (ms_mins / 1e3)
-    traffic = None
+    traffic = issue_busy = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
-            traffic = json.load(fh).get("bytes_per_launch")
+            tj = json.load(fh)
+            traffic = tj.get("bytes_per_launch")
+            issue_busy = tj.get("issue_slots_busy")
     share = ms_mins / (sum(l[0] for l in launch_ms) / args.steps)
 
     # ---- CPU baseline on a bounded sample + per-frame parity on that sample ----
@@ -368,7 +370,8 @@ def run_ours(args, rank, world, local_rank):
                      "kernel": "qsg::decode_kernel<5,32,false,false,256> (min-sum family, marginal VN, n_pad 256)",
                      "ops_per_cn_edge_update": "SURVEY.md 8(d): SAGMS 34.3, SMS 34.0",
                      "peak_basis": "148 SMs x 128 lane-instr/clk x measured median SM clock",
-                     "share_of_step": share},
+                     "share_of_step": share,
+                     "ncu_issue_slots_busy": issue_busy},
         "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": int(e2e_h2d),
                 "d2h_bytes_per_step": int(e2e_d2h),
                 "api": "decode_host_batches: uint8 syndromes (reference decode_batch format) in pinned host "

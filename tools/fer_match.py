@@ -46,37 +46,55 @@ def gpu(frames, out):
                                    gain=P.GainParams(0.30, 0.50, 1.10) if c.gain else None)
             f, it = P.decode_frames(g, dcfg, p, p, 0, 0, frames)
             res[f"{name}@{p}/fails"] = f
-            res[f"{name}@{p}/iters"] = it
+            res[f"{name}@{p}/iters"] = it.astype(np.uint8)  # <= l_max = 100
     np.savez_compressed(out, **res)
 
 
-def cpu(frames, gpu_npz, out):
+def cpu(frames, gpu_npz, out, nthreads=None, fp32=True):
+    """fp64 oracle on the same frames; rows are written after every point so
+    a long run can be inspected (and is kept) while it progresses."""
     from oracle import oracle as O
     from paper_2605_10433_b200.harness import wilson_interval
     g = O.Graph(O.gb_graph(*CODE))
     d = np.load(gpu_npz)
     rows = []
+
+    def dump(done):
+        summary = {"points": len(rows), "complete": done,
+                   "all_gpu_fer_in_ref_ci": all(r["gpu_fer_in_ref_ci"] for r in rows),
+                   "total_flipped_frames": sum(r["frames_flipped"] for r in rows),
+                   "total_frames": sum(r["frames"] for r in rows)}
+        if fp32:
+            summary["all_gpu_equal_fp32_oracle"] = all(r["gpu_equals_fp32_oracle"] for r in rows)
+        with open(out, "w") as fh:
+            json.dump({"summary": summary, "rows": rows}, fh, indent=1)
+        return summary
+
+    kw = {"nthreads": nthreads} if nthreads else {}
     for p in PS:
         for name in NAMES:
             gf = d[f"{name}@{p}/fails"][:frames]
-            of, oit, _, _ = O.frames(g, cfg_ns(name), p, p, 0, 0, frames, precision=64)
-            o32, _, _, _ = O.frames(g, cfg_ns(name), p, p, 0, 0, frames, precision=32)
+            git = d[f"{name}@{p}/iters"][:frames].astype(np.int64)
+            of, oit, _, _ = O.frames(g, cfg_ns(name), p, p, 0, 0, frames, precision=64, **kw)
             n = len(gf)
             fg, fo = int(gf.sum()), int(of.sum())
             lg, hg = wilson_interval(fg, n)
             lo, ho = wilson_interval(fo, n)
-            rows.append({"point": f"{name}@{p}", "frames": n, "gpu_failures": fg, "ref64_failures": fo,
-                         "gpu_fer": fg / n, "ref64_fer": fo / n, "gpu_wilson95": [lg, hg],
-                         "ref64_wilson95": [lo, ho], "gpu_fer_in_ref_ci": lo <= fg / n <= ho,
-                         "frames_flipped": int((gf != of).sum()),
-                         "gpu_equals_fp32_oracle": bool(np.array_equal(gf, o32))})
-    summary = {"points": len(rows), "all_gpu_fer_in_ref_ci": all(r["gpu_fer_in_ref_ci"] for r in rows),
-               "all_gpu_equal_fp32_oracle": all(r["gpu_equals_fp32_oracle"] for r in rows),
-               "total_flipped_frames": sum(r["frames_flipped"] for r in rows),
-               "total_frames": sum(r["frames"] for r in rows)}
-    with open(out, "w") as fh:
-        json.dump({"summary": summary, "rows": rows}, fh, indent=1)
-    print(json.dumps(summary))
+            row = {"point": f"{name}@{p}", "frames": n, "gpu_failures": fg, "ref64_failures": fo,
+                   "gpu_fer": fg / n, "ref64_fer": fo / n, "gpu_wilson95": [lg, hg],
+                   "ref64_wilson95": [lo, ho], "gpu_fer_in_ref_ci": lo <= fg / n <= ho,
+                   "frames_flipped": int((gf != of).sum()),
+                   "gpu_only_failures": int((gf & ~of.astype(bool)).sum()),
+                   "ref64_only_failures": int((~gf.astype(bool) & of.astype(bool)).sum()),
+                   "frames_iterations_differ": int((git != oit).sum()),
+                   "mean_iterations_gpu": float(git.mean()), "mean_iterations_ref64": float(oit.mean())}
+            if fp32:
+                o32, _, _, _ = O.frames(g, cfg_ns(name), p, p, 0, 0, frames, precision=32, **kw)
+                row["gpu_equals_fp32_oracle"] = bool(np.array_equal(gf, o32))
+            rows.append(row)
+            dump(False)
+            print(row["point"], fg, fo, row["gpu_fer_in_ref_ci"], flush=True)
+    print(json.dumps(dump(True)))
 
 
 if __name__ == "__main__":
@@ -85,8 +103,10 @@ if __name__ == "__main__":
     ap.add_argument("--frames", type=int, default=32768)
     ap.add_argument("--gpu-npz", default=os.path.join(ROOT, "gpurun_out", "fer_gpu.npz"))
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "fer_match_r01.json"))
+    ap.add_argument("--threads", type=int, default=None)
+    ap.add_argument("--no-fp32", action="store_true", help="skip the fp32-oracle equality column")
     a = ap.parse_args()
     if a.mode == "gpu":
         gpu(a.frames, a.gpu_npz)
     else:
-        cpu(a.frames, a.gpu_npz, a.out)
+        cpu(a.frames, a.gpu_npz, a.out, nthreads=a.threads, fp32=not a.no_fp32)
