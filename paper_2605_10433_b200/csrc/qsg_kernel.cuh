@@ -516,16 +516,22 @@ __device__ __forceinline__ void bitmaps_from_bytes(const KParams &p, const Group
 // clipped magnitudes are min(min1, 64), min(min2, 64) (clip is monotone),
 // with the |v_e| == min1 test unchanged whenever min1 < 64 and irrelevant
 // (min2 == min1 == 64) otherwise.
-template <int D, bool BP4>
-__device__ __forceinline__ void cn_update_fixed(const uint16_t *row, uint32_t msg_s, uint32_t sneg, float gain)
+// Split into the loads and the update so that callers can issue the loads
+// of a second check before the first one's stores (the shared accesses are
+// volatile asm, kept in program order).
+template <int D>
+__device__ __forceinline__ void cn_load(const uint16_t *row, uint32_t msg_s, uint32_t (&ad)[D], float (&v)[D])
 {
-    uint32_t ad[D];
-    float v[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) {
         ad[k] = msg_s + 4u * lds_u16(row + k);  // bicycle rows hold u16 slot indices
         v[k] = lds_a(ad[k]);
     }
+}
+
+template <int D, bool BP4>
+__device__ __forceinline__ void cn_finish(const uint32_t (&ad)[D], const float (&v)[D], uint32_t sneg, float gain)
+{
     if constexpr (BP4) {
         uint32_t sx = sneg;
 #pragma unroll
@@ -625,6 +631,15 @@ __device__ __forceinline__ void cn_update_fixed(const uint16_t *row, uint32_t ms
     }
 }
 
+template <int D, bool BP4>
+__device__ __forceinline__ void cn_update_fixed(const uint16_t *row, uint32_t msg_s, uint32_t sneg, float gain)
+{
+    uint32_t ad[D];
+    float v[D];
+    cn_load<D>(row, msg_s, ad, v);
+    cn_finish<D, BP4>(ad, v, sneg, gain);
+}
+
 // Inline both circulant halves (check c and l + c, qubit c and l + c) in the
 // min-sum kernels (more independent work per lane; +4-5% on the 128-thread
 // kernels once the paired math made the qubit update short).  BP4 (20
@@ -652,8 +667,17 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, u
                                             msg_s, sy << 31, (rs & 1u) ? g1 : g0);
             };
             if constexpr (kUnrollPair<T, BP4>) {
-                one(0);
-                one(1);
+                // both checks' loads first, then the two updates
+                constexpr int D = 2 * W;
+                const int wd0 = c >> 5, wd1 = nw + (c >> 5);
+                const uint32_t s0 = gm.synw[wd0] >> bit, r0 = gm.resw[wd0] >> bit;
+                const uint32_t s1 = gm.synw[wd1] >> bit, r1 = gm.resw[wd1] >> bit;
+                uint32_t ad0[D], ad1[D];
+                float v0[D], v1[D];
+                cn_load<D>(reinterpret_cast<const uint16_t *>(gm.tab + c * p.row_words), msg_s, ad0, v0);
+                cn_load<D>(reinterpret_cast<const uint16_t *>(gm.tab + (l + c) * p.row_words), msg_s, ad1, v1);
+                cn_finish<D, BP4>(ad0, v0, s0 << 31, (r0 & 1u) ? g1 : g0);
+                cn_finish<D, BP4>(ad1, v1, s1 << 31, (r1 & 1u) ? g1 : g0);
             } else {
 #pragma unroll 1
                 for (int h = 0; h < 2; ++h) one(h);
@@ -728,17 +752,23 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, u
 // reference's literal per-edge form).  Returns the hard decision.
 // NP > 0: the qubit stride n_pad is a compile-time constant, so the D column
 // loads / stores use immediate offsets from one base (no address IMADs).
+template <int W, int NP>
+__device__ __forceinline__ void vn_load(uint32_t cs, uint32_t rowb, float (&c)[2 * W])
+{
+    if constexpr (NP > 0) rowb = 4u * NP;
+#pragma unroll
+    for (int s = 0; s < 2 * W; ++s) c[s] = lds_a(cs + s * rowb);
+}
+
 template <int W, bool ADD, int NP>
-__device__ __forceinline__ uint32_t vn_update_fixed(unsigned char *col, uint32_t rowb, float l0, float kapc)
+__device__ __forceinline__ uint32_t vn_finish(uint32_t cs, uint32_t rowb, const float (&c)[2 * W], float l0,
+                                              float kapc)
 {
     if constexpr (NP > 0) rowb = 4u * NP;
     constexpr int D = 2 * W;
-    const uint32_t cs = smem_addr(col);
-    float c[D];
     OptF ox[D], oz[D], oa[D];
 #pragma unroll
     for (int s = 0; s < D; ++s) {
-        c[s] = lds_a(cs + s * rowb);
         // anti_X keeps Z-edges (z-bit), anti_Z keeps X-edges (x-bit)
         ox[s] = OptF{c[s], s >= W};
         oz[s] = OptF{c[s], s < W};
@@ -765,6 +795,15 @@ __device__ __forceinline__ uint32_t vn_update_fixed(unsigned char *col, uint32_t
         }
     }
     return hard_decision(bX, bZ, bY);
+}
+
+template <int W, bool ADD, int NP>
+__device__ __forceinline__ uint32_t vn_update_fixed(unsigned char *col, uint32_t rowb, float l0, float kapc)
+{
+    const uint32_t cs = smem_addr(col);
+    float c[2 * W];
+    vn_load<W, NP>(cs, rowb, c);
+    return vn_finish<W, ADD, NP>(cs, rowb, c, l0, kapc);
 }
 
 template <int W, int T, bool BP4, bool ADD, int NP>
