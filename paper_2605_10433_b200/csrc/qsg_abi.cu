@@ -184,12 +184,19 @@ int compile_layout(qsg_graph *g, int32_t n, int32_t m, const int64_t *cn_ptr, co
             }
         }
     }
-    // threads per frame: every thread owns <= 32 checks (register bit masks);
-    // bicycle kernels own circulant indices (at most 4 per thread)
+    // threads per frame: every thread of a generic kernel owns <= 32 checks
+    // (register bit masks)
     const int nodes = std::max(n, m);
     if (nodes <= 32 * 12) g->threads = 32;
     else if (m <= 128 * 32) g->threads = 128;
     else return fail(QSG_EUNSUPPORTED, "more than 4096 checks");
+    // bicycle kernels: about four circulant indices per thread (measured:
+    // l = 127 fastest on 32 threads, l = 160-255 on 64, l = 320-511 on 128)
+    if (kind > 0) g->threads = g->ell <= 128 ? 32 : (g->ell <= 256 ? 64 : 128);
+    if (const char *env = std::getenv("QSG_THREADS")) {  // diagnostics: force 32 / 64 / 128 (bicycle)
+        const int t = std::atoi(env);
+        if (kind > 0 && (t == 32 || t == 64 || t == 128)) g->threads = t;
+    }
     if (kind > 0) {
         g->nw = (g->ell + 31) / 32;
         const int lpw = g->threads / (2 * g->nw);  // lanes per syndrome word
@@ -334,7 +341,7 @@ int launch_cfg(qsg_graph *g, bool bp4, bool add, void *fn, qsg::LaunchCfg *out)
     int max_smem = 0;
     QSG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
     const int T = g->threads;
-    int gmax = T == 32 ? 20 : 5;  // __launch_bounds__(640)
+    int gmax = 640 / T;           // __launch_bounds__(640)
     int cap_sm = 1 << 30;         // QSG_MAX_FRAMES_PER_SM: tuning/diagnostics only
     if (const char *env = std::getenv("QSG_MAX_FRAMES_PER_SM")) cap_sm = std::max(1, std::atoi(env));
     qsg::LaunchCfg best;

@@ -31,6 +31,8 @@ void *QSG_FN(QSG_W)(int T, bool bp4, bool add, int np)
     if (T == 32 && np == 256) return pick<32, 256>(bp4, add);
     if (T == 32 && np == 128) return pick<32, 128>(bp4, add);
     if (T == 128 && np == 512) return pick<128, 512>(bp4, add);
+    if (T == 64 && np == 512) return pick<64, 512>(bp4, add);
+    if (T == 64) return pick<64, 0>(bp4, add);
     if (T == 128 && np == 1024) return pick<128, 1024>(bp4, add);
     if (T == 32) return pick<32, 0>(bp4, add);
     if (T == 128) return pick<128, 0>(bp4, add);

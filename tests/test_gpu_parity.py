@@ -239,14 +239,19 @@ def test_decode_host_batches_pipeline(P, oracle):
         assert np.array_equal(iters.numpy(), w.iterations)
 
 
-@pytest.mark.parametrize("ell,w", [(160, 5), (600, 4)])
-def test_unplanned_syndrome_shapes_bit_exact(P, oracle, ell, w):
-    """Bicycle shapes with fewer than 4 lanes per syndrome word (l = 160 on
-    one warp, l = 600 on 128 threads) take the generic circ_syndrome path
-    instead of the per-lane window plan; both must match the oracle."""
+@pytest.mark.parametrize("ell,w,threads", [(160, 5, 32), (600, 4, None)])
+def test_unplanned_syndrome_shapes_bit_exact(P, oracle, monkeypatch, ell, w, threads):
+    """Bicycle shapes with fewer than 4 lanes per syndrome word (l = 160
+    forced onto one warp, l = 600 on 128 threads) take the generic
+    circ_syndrome path instead of the per-lane window plan; both must match
+    the oracle."""
+    if threads:
+        monkeypatch.setenv("QSG_THREADS", str(threads))
     spec = P.random_gb_spec(ell, w, seed=1)
     g = P.gb_graph(spec)
     assert g.kind == w
+    if threads:
+        assert P.device_graph(g).threads == threads
     for variant, kw in CFGS:
         cfg = _cfg(P, variant, kw, l_max=25)
         fails, iters, ehat = P.decode_frames_device(g, cfg, 0.07, 0.07, 3, 0, 64, want_ehat=True)
