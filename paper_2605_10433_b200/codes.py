@@ -62,6 +62,7 @@ class CodeGraph:
     vn_order: np.ndarray = field(repr=False)
     vn_ptr: np.ndarray = field(repr=False)
     kind: int = 0
+    threads: int = 0  # threads per frame of the kernel the layout compiler picked
     gb: GbSpec | None = None
 
     @property
@@ -122,7 +123,7 @@ def _export(handle, gb=None) -> CodeGraph:
         vn_order=np.zeros(E.value, np.int64), vn_ptr=np.zeros(n.value + 1, np.int64),
     )
     _native.check(L.qsg_graph_export(handle, *(a.ctypes.data for a in arrs.values())))
-    return CodeGraph(n=n.value, m=m.value, kind=kind.value, gb=gb, **arrs)
+    return CodeGraph(n=n.value, m=m.value, kind=kind.value, threads=thr.value, gb=gb, **arrs)
 
 
 def _with_host_handle(create):

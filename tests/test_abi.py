@@ -61,6 +61,16 @@ def test_layout_compiler_host_only(oracle, spec, kind):
     assert g.kind == kind
 
 
+@pytest.mark.parametrize("ell,threads", [(63, 32), (127, 32), (128, 32), (129, 64), (255, 64), (256, 64),
+                                         (257, 128), (511, 128)])
+def test_threads_per_frame_rule(ell, threads):
+    """Bicycle kernels use about four circulant indices per thread: 32
+    threads for l <= 128, 64 for l <= 256, else 128."""
+    import paper_2605_10433_b200 as P
+    g = P.gb_graph(P.GbSpec(ell, (0, 1, 3, 7, 12), (0, 2, 5, 9, 14)))
+    assert g.kind == 5 and g.threads == threads
+
+
 def test_layout_compiler_vs_reference(reference):
     import paper_2605_10433_b200 as P
     from qsagms.code import GbSpec, build_gb, load_code, tanner_graph
