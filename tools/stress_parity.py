@@ -15,7 +15,7 @@ rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
 cases = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 bad = 0
 for i in range(cases):
-    ell = int(rng.choice([33, 47, 63, 64, 96, 127, 128, 150, 191, 255, 300, 511, 512]))
+    ell = int(rng.choice([33, 47, 63, 64, 96, 127, 128, 129, 150, 191, 200, 255, 256, 257, 300, 511, 512]))
     w = int(rng.choice([2, 3, 4, 5, 6, 8]))
     if w >= ell // 2:
         continue
@@ -59,7 +59,7 @@ for i in range(cases):
     ok = (np.array_equal(f.cpu().numpy().astype(bool), of) and np.array_equal(it.cpu().numpy(), oi)
           and np.array_equal(eh.cpu().numpy(), oe))
     bad += not ok
-    print(f"{'ok ' if ok else 'BAD'} l={ell} w={w} kind={g.kind} {variant} {cfg.vn_mode} l_max={cfg.l_max} "
+    print(f"{'ok ' if ok else 'BAD'} l={ell} w={w} kind={g.kind} T={g.threads} {variant} {cfg.vn_mode} l_max={cfg.l_max} "
           f"p={p:.3f} frames={count}", flush=True)
 print("STRESS_FAILURES", bad)
 sys.exit(1 if bad else 0)
