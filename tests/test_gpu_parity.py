@@ -167,7 +167,7 @@ def test_persistent_queue_partition_invariance(P):
 
 
 # BASELINE configs 3-4 codes: every bicycle kernel instantiation (W = 3, 4, 5,
-# 6, 8; T = 32 and 128) against the oracle, bit for bit.
+# 6, 8; T = 32, 64 and 128) against the oracle, bit for bit.
 CONFIG34_CODES = [(127, 3), (127, 4), (127, 6), (127, 8), (63, 5), (255, 5), (511, 5)]
 
 
@@ -177,6 +177,7 @@ def test_config34_codes_bit_exact(P, oracle, ell, w, vn_mode):
     spec = P.random_gb_spec(ell, w, seed=0)
     g = P.gb_graph(spec)
     assert g.kind == w
+    assert g.threads == (32 if ell <= 128 else (64 if ell <= 256 else 128))
     B = 96 if ell >= 255 else 160
     for variant, kw in CFGS:
         cfg = _cfg(P, variant, kw, l_max=30, vn_mode=vn_mode)
