@@ -333,6 +333,17 @@ def run_ours(args, rank, world, local_rank):
             traffic = tj.get("bytes_per_launch")
             issue_busy = tj.get("issue_slots_busy")
     share = ms_mins / (sum(l[0] for l in launch_ms) / args.steps)
+    # the BP4 launches (the rest of the step), against the same issue roof
+    # and against SURVEY 8(d)'s MUFU-class roof for BP4 (10 of its 44.1 ops)
+    bp4s = [k for k, (name, _, _) in enumerate(points) if name == "bp4"]
+    ms_bp4 = sum(launch_ms[k][0] for k in bp4s) / args.steps
+    upd_bp4 = sum(cnt[k, 3] / world for k in bp4s)
+    bp4_line = {"achieved": upd_bp4 * OPS_PER_EDGE["bp4"] / (ms_bp4 / 1e3) / 1e9, "peak": peak / 1e9,
+                "unit": "Gop/s", "frac": upd_bp4 * OPS_PER_EDGE["bp4"] / (ms_bp4 / 1e3) / peak,
+                "cn_edge_updates_per_s": upd_bp4 / (ms_bp4 / 1e3),
+                "frac_of_mufu_roof": (upd_bp4 / (ms_bp4 / 1e3)) / (dg_sms() * 16 * f_sm / 10),
+                "kernel": "qsg::decode_kernel<5,32,true,false,256> (BP4, marginal VN)",
+                "share_of_step": ms_bp4 / (sum(l[0] for l in launch_ms) / args.steps)}
 
     # ---- CPU baseline on a bounded sample + per-frame parity on that sample ----
     cpu = {}
@@ -372,6 +383,7 @@ def run_ours(args, rank, world, local_rank):
                      "peak_basis": "148 SMs x 128 lane-instr/clk x measured median SM clock",
                      "share_of_step": share,
                      "ncu_issue_slots_busy": issue_busy},
+        "roofline_bp4": bp4_line,
         "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": int(e2e_h2d),
                 "d2h_bytes_per_step": int(e2e_d2h),
                 "api": "decode_host_batches: uint8 syndromes (reference decode_batch format) in pinned host "
