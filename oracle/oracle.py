@@ -73,6 +73,7 @@ def lib():
             getattr(L, f"qsgo{p}_frames").argtypes = [vp, vp, dbl, dbl, u64, i64, i64,
                                                       vp, vp, vp, vp, i32]
         L.qsgo_math32_batch.argtypes = [i32, vp, vp, vp, i64]
+        L.qsgo_bp4_mags.argtypes = [vp, i32, vp]
         _lib = L
     return _lib
 
@@ -253,7 +254,7 @@ def prior_llr(epsilon0):
     return math.log(3.0 * (1.0 - epsilon0) / epsilon0)
 
 
-MATH_FUNCS = {"exp_neg": 0, "log1p_01": 1, "log1p": 2, "expm1": 3, "logaddexp": 4, "phi": 5, "vnF": 6}
+MATH_FUNCS = {"exp_neg": 0, "log1p_01": 1, "log1p": 2, "expm1": 3, "logaddexp": 4, "vnF": 6}
 
 
 def math32(name, x, y=None):
@@ -261,4 +262,13 @@ def math32(name, x, y=None):
     y = np.ascontiguousarray(y if y is not None else x, dtype=np.float32)
     out = np.empty_like(x)
     lib().qsgo_math32_batch(MATH_FUNCS[name], _ptr(x), _ptr(y), _ptr(out), x.size)
+    return out
+
+
+def bp4_mags(x):
+    """Output magnitudes of one BP4 check for input magnitudes x (the fp32
+    product-form recipe, qo_bp4_mags)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.empty_like(x)
+    lib().qsgo_bp4_mags(_ptr(x), x.size, _ptr(out))
     return out

@@ -102,10 +102,10 @@ void qsgo_syndromes_of(const qsgo_graph *g, const uint8_t *e, int64_t B, uint8_t
 #define SFX 32
 #define TRACE_T qsgo_trace32
 #define LAE(x, y) qo_logaddexp((x), (y))
-#define PHI(x) qo_phi(x)
 #define MAXR(a, b) fmaxf((a), (b))
 #define ABSR(x) fabsf(x)
 #define VN_FACTORED 1
+#define BP4_PRODUCT 1
 #include "qsg_oracle_body.h"
 #undef REAL
 #undef SFX
@@ -115,6 +115,7 @@ void qsgo_syndromes_of(const qsgo_graph *g, const uint8_t *e, int64_t B, uint8_t
 #undef MAXR
 #undef ABSR
 #undef VN_FACTORED
+#undef BP4_PRODUCT
 
 /* ---- fp64 with glibc: the reference's own arithmetic ---- */
 static inline double lae64(double x, double y) /* npy_logaddexp */
@@ -132,7 +133,14 @@ static inline double lae64(double x, double y) /* npy_logaddexp */
 #define MAXR(a, b) fmax((a), (b))
 #define ABSR(x) fabs(x)
 #define VN_FACTORED 0
+#define BP4_PRODUCT 0
 #include "qsg_oracle_body.h"
+
+/* One BP4 check: output magnitudes for input magnitudes x[0..d) (fp32 recipe). */
+void qsgo_bp4_mags(const float *x, int32_t d, float *out)
+{
+    if (d >= 1 && d <= QO_BP4_MAXD) qo_bp4_mags(x, (int)d, out);
+}
 
 void qsgo_math32_batch(int32_t which, const float *x, const float *y, float *out, int64_t n)
 {
@@ -143,7 +151,6 @@ void qsgo_math32_batch(int32_t which, const float *x, const float *y, float *out
         case 2: out[i] = qo_log1p(x[i]); break;
         case 3: out[i] = qo_expm1(x[i]); break;
         case 4: out[i] = qo_logaddexp(x[i], y[i]); break;
-        case 5: out[i] = qo_phi(x[i]); break;
         case 6: out[i] = qo_vnF(x[i], qo_vn_kapc(y[i])); break;
         default: out[i] = NAN;
         }

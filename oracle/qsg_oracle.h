@@ -80,6 +80,7 @@ int qsgo64_frames(const qsgo_graph *g, const qsgo_cfg *cfg, double epsilon,
 /* fp32 recipe entry points, exposed so tests can measure their accuracy and
  * compare them with the CUDA copy. */
 void qsgo_math32_batch(int32_t which, const float *x, const float *y, float *out, int64_t n);
+void qsgo_bp4_mags(const float *x, int32_t d, float *out);
 
 #ifdef __cplusplus
 }

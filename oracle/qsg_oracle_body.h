@@ -136,6 +136,17 @@ static void QF(_decode_one)(const qsgo_graph *g, const qsgo_cfg *cfg, REAL l0, R
             REAL prod = (REAL)1.0;
             for (int64_t q = 0; q < d; ++q) prod *= (s->vmsg[p0 + q] < (REAL)0.0) ? (REAL)-1.0 : (REAL)1.0;
             if (cfg->variant == 0) { /* bp4 :318-323 */
+#if BP4_PRODUCT
+                /* fp32 restatement: the same magnitudes in the product
+                 * domain (qo_bp4_mags); vmsg is clipped to +-64 already */
+                for (int64_t q = 0; q < d; ++q) s->ph[q] = ABSR(s->vmsg[p0 + q]);
+                qo_bp4_mags(s->ph, (int)d, s->tmp);
+                for (int64_t q = 0; q < d; ++q) {
+                    REAL v = s->vmsg[p0 + q];
+                    REAL sg = (v < (REAL)0.0) ? (REAL)-1.0 : (REAL)1.0;
+                    s->cmsg[p0 + q] = QF(_clip)((syn_sign * prod) * sg * s->tmp[q], -CLIP, CLIP);
+                }
+#else
                 for (int64_t q = 0; q < d; ++q)
                     s->ph[q] = PHI(MAXR(ABSR(s->vmsg[p0 + q]), (REAL)1e-12));
                 REAL total = QF(_segsum)(s->ph, d);
@@ -146,6 +157,7 @@ static void QF(_decode_one)(const qsgo_graph *g, const qsgo_cfg *cfg, REAL l0, R
                     REAL mag = PHI(ext);
                     s->cmsg[p0 + q] = QF(_clip)((syn_sign * prod) * sg * mag, -CLIP, CLIP);
                 }
+#endif
             } else { /* min-sum family :324-337 */
                 REAL min1 = (REAL)INFINITY;
                 for (int64_t q = 0; q < d; ++q) {

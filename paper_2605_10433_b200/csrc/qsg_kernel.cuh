@@ -9,7 +9,8 @@
 //   for ell = 1..l_max (decoder.py:422-469):
 //     R: residual = syndrome ^ synd(e_hat), unsat via popc + group reduce
 //     exit on success / l_max; SAGMS gains from gamma (decoder.py:462-467)
-//     C: check-node update (min1/min2/sign or BP4 phi), decoder.py:311-338
+//     C: check-node update (min1/min2/sign, or BP4 in the product domain),
+//        decoder.py:311-338
 //     V: qubit-node update (marginal or additive), decoder.py:340-359, which
 //        also produces the next iteration's hard decision (the reduceat sums
 //        of hard_decisions, decoder.py:292-301, are the same sums).
@@ -533,75 +534,18 @@ template <int D, bool BP4>
 __device__ __forceinline__ void cn_finish(const uint32_t (&ad)[D], const float (&v)[D], uint32_t sneg, float gain)
 {
     if constexpr (BP4) {
+        // product-form magnitudes (qsg_math.cuh bp4_mags, paired:
+        // bp4_mags_fixed); the sign as in the min-sum branch
         uint32_t sx = sneg;
 #pragma unroll
         for (int k = 0; k < D; ++k) sx ^= f2u(v[k]);
         const uint32_t sgn = sx & 0x80000000u;  // (-1)^s_i * prod sgn, as a sign bit
-        // The forward phi(|v|) is evaluated on the x >= ln2 side only when
-        // every active lane of the warp has all its arguments there (a
-        // warp-uniform branch, the common case); otherwise, and always for
-        // the extrinsic phi (whose arguments straddle ln 2 in most warps,
-        // measured), both sides with a select.
-        const unsigned act = __activemask();
-        float x[D], ph[D];
-        float xmin = kClip;
+        float x[D], mag[D];
 #pragma unroll
-        for (int k = 0; k < D; ++k) {
-            x[k] = fmaxf(fminf(fabsf(v[k]), kClip), 1e-12f);
-            xmin = fminf(xmin, x[k]);
-        }
-        // phi on edge pairs (k, k+1): FFMA2 / FADD2 / FMUL2 (qsg_math2.cuh)
-        static_assert(D % 2 == 0, "bicycle checks have even degree");
-        if (__all_sync(act, xmin >= kLn2f)) {
+        for (int k = 0; k < D; ++k) x[k] = fminf(fabsf(v[k]), kClip);
+        bp4_mags_fixed<D>(x, mag);
 #pragma unroll
-            for (int k = 0; k < D; k += 2) {
-                const F2 y = phi_hi2(pk(x[k], x[k + 1]));
-                ph[k] = lo(y); ph[k + 1] = hi(y);
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < D; k += 2) {
-                const F2 y = phi2(pk(x[k], x[k + 1]));
-                ph[k] = lo(y); ph[k + 1] = hi(y);
-            }
-        }
-        OptF o[D];
-#pragma unroll
-        for (int k = 0; k < D; ++k) o[k] = OptF{ph[k], true};
-        const float total = segsum_c<D>(o);
-        float r[D], ex[D];
-        float emin = 50.0f, emax = 0.0f;
-#pragma unroll
-        for (int k = 0; k < D; k += 2) {
-            const F2 e = sub2(bc(total), pk(ph[k], ph[k + 1]));
-            ex[k] = fminf(fmaxf(lo(e), 1e-12f), 50.0f);
-            ex[k + 1] = fminf(fmaxf(hi(e), 1e-12f), 50.0f);
-            emin = fminf(emin, fminf(ex[k], ex[k + 1]));
-            emax = fmaxf(emax, fmaxf(ex[k], ex[k + 1]));
-        }
-        // extrinsic phi: one side only when the whole warp is there (most
-        // warps at low p sit below ln 2), else both sides (paired)
-        if (__all_sync(act, emax < kLn2f)) {
-#pragma unroll
-            for (int k = 0; k < D; k += 2) {
-                const F2 y = phi_lo2(pk(ex[k], ex[k + 1]));
-                r[k] = lo(y); r[k + 1] = hi(y);
-            }
-        } else if (__all_sync(act, emin >= kLn2f)) {
-#pragma unroll
-            for (int k = 0; k < D; k += 2) {
-                const F2 y = phi_hi2(pk(ex[k], ex[k + 1]));
-                r[k] = lo(y); r[k + 1] = hi(y);
-            }
-        } else {
-#pragma unroll
-            for (int k = 0; k < D; k += 2) {
-                const F2 y = phi2(pk(ex[k], ex[k + 1]));
-                r[k] = lo(y); r[k + 1] = hi(y);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < D; ++k) sts_a(ad[k], (f2u(v[k]) & 0x80000000u) ^ f2u(fminf(r[k], kClip)) ^ sgn);
+        for (int k = 0; k < D; ++k) sts_a(ad[k], (f2u(v[k]) & 0x80000000u) ^ f2u(mag[k]) ^ sgn);
     } else {
         // smallest and second smallest of |v| (with multiplicity), two at a
         // time: second' = min(second, max(min1, lo), hi).  min1 carries the
@@ -705,23 +649,36 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, u
             }
             const uint32_t sgn = sx & 0x80000000u;
             if constexpr (BP4) {
-                float ph[DM], r[DM];
+                // product-form magnitudes (qsg_math.cuh bp4_mags) for the
+                // run-time degree d <= DM: the prefix (A, B) is kept per
+                // edge, the suffix runs backwards alongside the merge (the
+                // scalar recipe's operations; unused steps predicated off)
+                uint32_t vs = 0;  // message sign bits
+                float s[DM], A[DM], B[DM];
 #pragma unroll
                 for (int k = 0; k < DM; k += 2) {
-                    const F2 y = phi2(pk(fmaxf(fminf(fabsf(v[k]), kClip), 1e-12f),
-                                         fmaxf(fminf(fabsf(v[k + 1]), kClip), 1e-12f)));
-                    ph[k] = lo(y); ph[k + 1] = hi(y);
+                    vs |= (f2u(v[k]) >> 31) << k | (f2u(v[k + 1]) >> 31) << (k + 1);
+                    const F2 e = exp_neg2(pk(-fminf(fabsf(v[k]), kClip), -fminf(fabsf(v[k + 1]), kClip)));
+                    s[k] = lo(e); s[k + 1] = hi(e);
                 }
-                const float total = segsum_pred<DM>(ph, d);
+                A[0] = 1.0f; B[0] = 0.0f;
 #pragma unroll
-                for (int k = 0; k < DM; k += 2) {
-                    const F2 e = sub2(bc(total), pk(ph[k], ph[k + 1]));
-                    const F2 y = phi2(pk(fminf(fmaxf(lo(e), 1e-12f), 50.0f), fminf(fmaxf(hi(e), 1e-12f), 50.0f)));
-                    r[k] = lo(y); r[k + 1] = hi(y);
+                for (int j = 0; j + 1 < DM; ++j) {
+                    const bool on = j + 1 < d;
+                    A[j + 1] = on ? fmaf(s[j], B[j], A[j]) : A[j];
+                    B[j + 1] = on ? fmaf(s[j], A[j], B[j]) : B[j];
                 }
+                float C = 1.0f, Dd = 0.0f;  // suffix of edge e (edges e+1 .. d-1)
 #pragma unroll
-                for (int k = 0; k < DM; ++k)
-                    if (k < d) sts_a(ad[k], (f2u(v[k]) & 0x80000000u) ^ f2u(fminf(r[k], kClip)) ^ sgn);
+                for (int e = DM - 1; e >= 0; --e) {
+                    if (e < d) {
+                        const F2 t = mul2(bc(B[e]), pk(Dd, C));
+                        const float mag = fminf(fmaxf(log_ratio2(fma2(bc(A[e]), pk(C, Dd), t)), kPhi50), kPhiTiny);
+                        sts_a(ad[e], ((vs >> e) << 31) ^ f2u(mag) ^ sgn);
+                        const float Cn = fmaf(s[e], Dd, C), Dn = fmaf(s[e], C, Dd);
+                        C = Cn; Dd = Dn;
+                    }
+                }
             } else {
                 float mn1 = __int_as_float(0x7f800000), mn2 = mn1;
 #pragma unroll

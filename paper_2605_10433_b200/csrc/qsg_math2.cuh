@@ -122,32 +122,49 @@ __device__ __forceinline__ F2 vn_F2(float y0, float y1, F2 kapc2)
     return fma2(sub2(bc(0.0f), q), log1p_01_poly2(q), log_pos2(A));
 }
 
-// phi_hi / phi_lo / phi on both halves (BP4).
-__device__ __forceinline__ F2 phi_hi2(F2 x)
+// log_ratio(E, O) with the two mantissa logarithms paired.
+__device__ __forceinline__ float log_ratio2(F2 EO)
 {
-    const F2 t = exp_neg2(sub2(bc(0.0f), x));
-    const F2 u = mul2(t, t);
-    F2 S = fma2(bc(0.15731367f), u, bc(0.06506128f));
-    S = fma2(S, u, bc(0.11467144f));
-    S = fma2(S, u, bc(0.1426422f));
-    S = fma2(S, u, bc(0.20000467f));
-    S = fma2(S, u, bc(0.3333333f));
-    const F2 tt = add2(t, t);
-    return fma2(mul2(tt, u), S, tt);
+    const uint32_t a = f2u(lo(EO)), b = f2u(hi(EO));
+    const float feE = u2f(kMagicBits + ((a >> 23) - 127u)) - kMagic;
+    const float feO = u2f(kMagicBits + ((b >> 23) - 127u)) - kMagic;
+    const F2 f = sub2(pk(u2f((a & 0x007fffffu) | 0x3f800000u), u2f((b & 0x007fffffu) | 0x3f800000u)), bc(1.0f));
+    const F2 r = log1p_01_2(f);
+    const float de = feE - feO;
+    return fmaf(de, kLn2Hi, fmaf(de, kLn2Lo, lo(r) - hi(r)));
 }
-__device__ __forceinline__ F2 phi_lo2(F2 x)
+
+// BP4 product-form magnitudes (qsg_math.cuh bp4_mags) for a check of
+// compile-time degree D (even): exponentials on edge pairs, the prefix and
+// suffix recurrences side by side on FFMA2 (prefix in the low half, suffix
+// in the high half), the per-edge merge as an FMUL2 + FFMA2 (E, O) pair and
+// log_ratio with its two mantissa logarithms paired.  Each half performs exactly the scalar
+// recipe's operations (bit-identical).
+template <int D>
+__device__ __forceinline__ void bp4_mags_fixed(const float (&x)[D], float (&mag)[D])
 {
-    const F2 lg = log_pos2(x);
-    const F2 v = mul2(x, x);
-    F2 H = fma2(bc(-2.4306313e-05f), v, bc(0.0003411371f));
-    H = fma2(H, v, bc(-0.0048610563f));
-    H = fma2(H, v, bc(0.083333336f));
-    return fma2(v, H, sub2(bc(kLn2f), lg));
-}
-__device__ __forceinline__ F2 phi2(F2 x)
-{
-    const F2 a = phi_hi2(x), b = phi_lo2(x);
-    return pk(lo(x) < kLn2f ? lo(b) : lo(a), hi(x) < kLn2f ? hi(b) : hi(a));
+    static_assert(D % 2 == 0, "paired exponentials need an even degree");
+    float s[D], A[D], B[D], C[D], Dd[D];
+#pragma unroll
+    for (int k = 0; k < D; k += 2) {
+        const F2 e = exp_neg2(pk(-x[k], -x[k + 1]));
+        s[k] = lo(e); s[k + 1] = hi(e);
+    }
+    A[0] = 1.0f; B[0] = 0.0f; C[D - 1] = 1.0f; Dd[D - 1] = 0.0f;
+    F2 P = bc(1.0f), Q = bc(0.0f);  // (A_j, C_{D-1-j}), (B_j, D_{D-1-j})
+#pragma unroll
+    for (int j = 0; j + 1 < D; ++j) {
+        const F2 S = pk(s[j], s[D - 1 - j]);
+        const F2 Pn = fma2(S, Q, P), Qn = fma2(S, P, Q);
+        P = Pn; Q = Qn;
+        A[j + 1] = lo(P); B[j + 1] = lo(Q); C[D - 2 - j] = hi(P); Dd[D - 2 - j] = hi(Q);
+    }
+#pragma unroll
+    for (int e = 0; e < D; ++e) {
+        const F2 t = mul2(bc(B[e]), pk(Dd[e], C[e]));            // (B D, B C)
+        const F2 EO = fma2(bc(A[e]), pk(C[e], Dd[e]), t);        // (E_e, O_e)
+        mag[e] = fminf(fmaxf(log_ratio2(EO), kPhi50), kPhiTiny);
+    }
 }
 
 }  // namespace qsg

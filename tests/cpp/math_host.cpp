@@ -14,9 +14,14 @@ extern "C" void qsg_math_host_batch(int32_t which, const float *x, const float *
         case 2: out[i] = qsg::log1p_pos(x[i]); break;
         case 3: out[i] = qsg::expm1_pos(x[i]); break;
         case 4: out[i] = qsg::logaddexp(x[i], y[i]); break;
-        case 5: out[i] = qsg::phi(x[i]); break;
         case 6: out[i] = qsg::vn_F(x[i], (float)exp(-(double)y[i])); break;  // kapc as the ABI computes it
         default: out[i] = 0.0f;
         }
     }
+}
+
+// One BP4 check: the product copy of the product-form magnitudes.
+extern "C" void qsg_bp4_host(const float *x, int32_t d, float *out)
+{
+    if (d >= 1 && d <= qsg::kBp4MaxDeg) qsg::bp4_mags(x, d, out);
 }

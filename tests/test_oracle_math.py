@@ -19,7 +19,7 @@ import numpy as np
 import pytest
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-FUNCS = {"exp_neg": 0, "log1p_01": 1, "log1p": 2, "expm1": 3, "logaddexp": 4, "phi": 5, "vnF": 6}
+FUNCS = {"exp_neg": 0, "log1p_01": 1, "log1p": 2, "expm1": 3, "logaddexp": 4, "vnF": 6}
 
 
 @pytest.fixture(scope="module")
@@ -29,12 +29,16 @@ def host_math(tmp_path_factory):
                     "-mfma", "-o", str(out), os.path.join(HERE, "cpp", "math_host.cpp")], check=True)
     lib = C.CDLL(str(out))
     lib.qsg_math_host_batch.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]
+    lib.qsg_bp4_host.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
 
     def run(name, x, y=None):
         x = np.ascontiguousarray(x, dtype=np.float32)
         y = np.ascontiguousarray(y if y is not None else x, dtype=np.float32)
         o = np.empty_like(x)
-        lib.qsg_math_host_batch(FUNCS[name], x.ctypes.data, y.ctypes.data, o.ctypes.data, x.size)
+        if name == "bp4":
+            lib.qsg_bp4_host(x.ctypes.data, x.size, o.ctypes.data)
+        else:
+            lib.qsg_math_host_batch(FUNCS[name], x.ctypes.data, y.ctypes.data, o.ctypes.data, x.size)
         return o
     return run
 
@@ -48,8 +52,6 @@ def _args(name, rng, n=200_000):
         return np.concatenate([10.0 ** rng.uniform(-30, 13, n), [0.0, 1.0, 0.999999]]), None
     if name == "expm1":
         return np.concatenate([rng.uniform(1e-12, 64, n), 10.0 ** rng.uniform(-12, 0, n // 2)]), None
-    if name == "phi":
-        return np.concatenate([rng.uniform(1e-12, 64, n), 10.0 ** rng.uniform(-12, 1.5, n // 2)]), None
     if name == "vnF":  # (y, l0): message sums over the decoder's range, priors of p in [1e-4, 0.7]
         p = 10.0 ** rng.uniform(-4, np.log10(0.7), n)
         l0 = np.log(3.0 * (1.0 - p) / p)
@@ -86,7 +88,7 @@ def _ulp_err(got, ref):
 
 
 @pytest.mark.parametrize("name,max_ulp", [("exp_neg", 2.0), ("log1p_01", 2.0), ("log1p", 2.5),
-                                          ("expm1", 3.0), ("phi", 3.0), ("logaddexp", 2.0)])
+                                          ("expm1", 3.0), ("logaddexp", 2.0)])
 def test_recipe_accuracy(oracle, name, max_ulp):
     L = _libm_long_double()
     rng = np.random.default_rng(99)
@@ -101,8 +103,6 @@ def test_recipe_accuracy(oracle, name, max_ulp):
         ref = np.array([float(L.log1pl(v)) for v in xs])
     elif name == "expm1":
         ref = np.array([float(L.expm1l(v)) for v in xs])
-    elif name == "phi":
-        ref = np.array([float(L.log1pl(2.0 / L.expm1l(v))) for v in xs])
     else:
         ys = y32.astype(np.float64)
         mx = np.maximum(xs, ys)
@@ -144,3 +144,61 @@ def test_exact_identities(oracle, host_math):
     x = np.float32([3.25, -7.5, 0.0, 64.0])
     assert np.array_equal(host_math("logaddexp", x, x), x + ln2f)
     assert np.array_equal(oracle.math32("logaddexp", x, x), x + ln2f)
+
+
+def _bp4_checks(rng, count):
+    """Random check inputs x_k = min(|v_k|, 64): degrees 1-32, a mix of
+    small (near-zero, the phi-sum's cancelling regime), moderate and large
+    magnitudes, exact zeros and the 64 clip."""
+    out = []
+    for _ in range(count):
+        d = int(rng.choice([1, 2, 3, 4, 6, 8, 10, 12, 16, 24, 32]))
+        kind = rng.random(d)
+        x = np.where(kind < 0.25, rng.exponential(0.05, d),
+                     np.where(kind < 0.5, rng.uniform(0.0, 3.0, d), rng.uniform(0.0, 64.0, d)))
+        x[rng.random(d) < 0.03] = 0.0
+        x[rng.random(d) < 0.03] = 64.0
+        out.append(x.astype(np.float32))
+    return out
+
+
+def test_bp4_product_and_oracle_recipes_bit_identical(oracle, host_math):
+    """The BP4 check recipe (qsg_math.cuh bp4_mags) and the oracle's copy
+    (qo_bp4_mags) agree bit for bit."""
+    for x in _bp4_checks(np.random.default_rng(5), 20_000):
+        a, b = oracle.bp4_mags(x), host_math("bp4", x)
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), x
+
+
+def test_bp4_check_accuracy(oracle):
+    """Product-form BP4 magnitudes against the exact value of the
+    reference's formula phi(clip(sum_k phi(x_k) - phi(x_e), 1e-12, 50))
+    (decoder.py:318-323, phi = log1p(2/expm1), inputs floored at 1e-12),
+    evaluated in 40-digit arithmetic: |err| <= 5e-7 max(|ref|, 1) (measured
+    1.7e-7; the float64 formula itself is off by 5.5e-6 here).  Against
+    the same formula in float64 -- the reference's own arithmetic, whose
+    sum - phi_e cancels when one small input dominates -- the agreement is
+    the north_star message tolerance, 1e-5 with the unit floor."""
+    import math
+    import mpmath as mp
+    mp.mp.dps = 40
+
+    def phi_mp(v):
+        return mp.log1p(2 / mp.expm1(mp.mpf(max(float(v), 1e-12))))
+
+    def phi_64(v):
+        return math.log1p(2.0 / math.expm1(max(float(v), 1e-12)))
+    worst = worst64 = 0.0
+    for x in _bp4_checks(np.random.default_rng(6), 1500):
+        got = oracle.bp4_mags(x).astype(np.float64)
+        ph = [phi_mp(v) for v in x]
+        tot = mp.fsum(ph)
+        p64 = [phi_64(v) for v in x]
+        t64 = sum(p64)
+        for e in range(len(x)):
+            ref = float(phi_mp(min(max(tot - ph[e], mp.mpf(1e-12)), 50)))
+            worst = max(worst, abs(got[e] - ref) / max(abs(ref), 1.0))
+            r64 = phi_64(min(max(t64 - p64[e], 1e-12), 50.0))
+            worst64 = max(worst64, abs(got[e] - r64) / max(abs(r64), 1.0))
+    assert worst <= 5e-7, worst
+    assert worst64 <= 1e-5, worst64

@@ -186,9 +186,16 @@ def test_fp32_messages_vs_reference_fp64(oracle, traces, cname, vn_mode, variant
 
 
 def test_bp4_closed_form(oracle):
-    """Reference test_decoder.py:105-112: two ln 3 inputs -> 2 atanh(1/4);
-    here through the fp32 phi recipe (fp32 tolerance)."""
-    ph = float(oracle.math32("phi", [math.log(3)])[0])
-    assert ph == pytest.approx(math.log(2), rel=2e-7)
-    out = float(oracle.math32("phi", [np.float32(ph) + np.float32(ph)])[0])
-    assert out == pytest.approx(2 * math.atanh(0.25), rel=4e-7)
+    """Reference test_decoder.py:105-112: a check whose other two inputs are
+    ln 3 sends 2 atanh(1/4) (tanh(ln3 / 2) = 1/2); here through the fp32
+    product-form recipe (fp32 tolerance), and each ln 3 edge receives
+    phi(phi(ln 3) + phi(x3))."""
+    x = np.float32([math.log(3), math.log(3), 5.0])
+    mag = oracle.bp4_mags(x)
+    assert float(mag[2]) == pytest.approx(2 * math.atanh(0.25), rel=4e-7)
+    t = math.tanh(math.log(3) / 2) * math.tanh(5.0 / 2)
+    assert float(mag[0]) == pytest.approx(2 * math.atanh(t), rel=4e-7)
+    # one input at 0 (tanh 0 = 0) silences the others; a lone edge gets the
+    # ext floor phi(1e-12)
+    assert np.all(oracle.bp4_mags(np.float32([0.0, 2.0, 3.0]))[1:] == np.float32(3.8574998e-22))
+    assert oracle.bp4_mags(np.float32([1.5]))[0] == np.float32(28.32417)

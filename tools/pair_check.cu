@@ -21,17 +21,23 @@ __global__ void k(const float* x, float* o, int n, int which) {
     case 1: s0 = log1p_01(a); s1 = log1p_01(b); r = log1p_01_2(pk(a, b)); break;
     case 2: s0 = log_pos(a); s1 = log_pos(b); r = log_pos2(pk(a, b)); break;
     case 3: s0 = vn_F(a, 0.03f); s1 = vn_F(b, 0.03f); r = vn_F2(a, b, bc(0.03f)); break;
-    case 4: s0 = phi_hi(a); s1 = phi_hi(b); r = phi_hi2(pk(a, b)); break;
-    case 5: s0 = phi_lo(a); s1 = phi_lo(b); r = phi_lo2(pk(a, b)); break;
-    case 6: s0 = phi(a); s1 = phi(b); r = phi2(pk(a, b)); break;
-    case 7: { // H(v) poly only
-      float v0 = a * a, v1 = b * b;
-      float H0 = -2.4306313e-05f; H0 = fmaf(H0, v0, 0.0003411371f); H0 = fmaf(H0, v0, -0.0048610563f); H0 = fmaf(H0, v0, 0.083333336f);
-      float H1 = -2.4306313e-05f; H1 = fmaf(H1, v1, 0.0003411371f); H1 = fmaf(H1, v1, -0.0048610563f); H1 = fmaf(H1, v1, 0.083333336f);
-      s0 = H0; s1 = H1;
-      F2 v = mul2(pk(a, b), pk(a, b));
-      F2 H = fma2(bc(-2.4306313e-05f), v, bc(0.0003411371f)); H = fma2(H, v, bc(-0.0048610563f)); H = fma2(H, v, bc(0.083333336f));
-      r = H; break; }
+    case 4: s0 = log_ratio(a, b); s1 = log_ratio(b, a); r = pk(log_ratio2(pk(a, b)), log_ratio2(pk(b, a))); break;
+    case 5: case 6: case 7: {  // one BP4 check (degree 10 / 10 / 6) from (a, b)
+      float x[10], ms[10], mp[10];
+      for (int q = 0; q < 10; ++q) x[q] = fminf(fabsf(a * (1.0f + q) - b * (3.0f - 0.7f * q)), 64.0f);
+      if (which == 7) {
+        float x6[6], m6[6];
+        for (int q = 0; q < 6; ++q) x6[q] = x[q];
+        bp4_mags(x, 6, ms);
+        bp4_mags_fixed<6>(x6, m6);
+        s0 = ms[0]; s1 = ms[5]; r = pk(m6[0], m6[5]);
+      } else {
+        bp4_mags(x, 10, ms);
+        bp4_mags_fixed<10>(x, mp);
+        const int q0 = which == 5 ? 0 : 4, q1 = which == 5 ? 9 : 5;
+        s0 = ms[q0]; s1 = ms[q1]; r = pk(mp[q0], mp[q1]);
+      }
+      break; }
     case 8: { // x*x * H-ish product and difference
       s0 = (kLn2f - a) + a * b; s1 = (kLn2f - b) + b * a;
       { F2 d = sub2(bc(kLn2f), pk(a, b)), m = mul2(pk(a, b), pk(b, a));
@@ -54,7 +60,7 @@ int main() {
   const int n = 1 << 20;
   float *h = new float[n], *ho = new float[2 * n];
   float *d, *dout; cudaMalloc(&d, n * 4); cudaMalloc(&dout, 2 * n * 4);
-  const char* names[] = {"exp_neg", "log1p_01", "log_pos", "vn_F", "phi_hi", "phi_lo", "phi", "Hpoly", "sub_add", "fma_imm", "mul", "add", "subc", "sub_add2"};
+  const char* names[] = {"exp_neg", "log1p_01", "log_pos", "vn_F", "log_ratio", "bp4_d10_ends", "bp4_d10_mid", "bp4_d6", "sub_add", "fma_imm", "mul", "add", "subc", "sub_add2"};
   int recipe_bad = 0;
   for (int w = 0; w < 14; ++w) {
     srand(1);
@@ -64,7 +70,8 @@ int main() {
       else if (w == 1) h[i] = u;
       else if (w == 2) h[i] = powf(10.0f, -30.0f + 32.0f * u);
       else if (w == 3) h[i] = -200.0f + 400.0f * u;
-      else if (w <= 6) h[i] = powf(10.0f, -12.0f + 13.8f * u);
+      else if (w == 4) h[i] = powf(10.0f, -30.0f + 60.0f * u);
+      else if (w <= 7) h[i] = powf(10.0f, -12.0f + 13.8f * u);
       else h[i] = -3.0f + 6.0f * u;
     }
     cudaMemcpy(d, h, n * 4, cudaMemcpyHostToDevice);
