@@ -575,22 +575,10 @@ __device__ __forceinline__ void cn_finish(const uint32_t (&ad)[D], const float (
     }
 }
 
-template <int D, bool BP4>
-__device__ __forceinline__ void cn_update_fixed(const uint16_t *row, uint32_t msg_s, uint32_t sneg, float gain)
-{
-    uint32_t ad[D];
-    float v[D];
-    cn_load<D>(row, msg_s, ad, v);
-    cn_finish<D, BP4>(ad, v, sneg, gain);
-}
-
-// Inline both circulant halves (check c and l + c, qubit c and l + c) in the
-// min-sum kernels (more independent work per lane; +4-5% on the 128-thread
-// kernels once the paired math made the qubit update short).  BP4 (20
-// inlined phi per check) keeps one copy in a loop: unrolled it overflows
-// the instruction cache (-25% measured).
-template <int T, bool BP4>
-constexpr bool kUnrollPair = !BP4;
+// Both circulant halves (check c and l + c, qubit c and l + c) are inlined:
+// more independent work per lane (+4-5% on the 128-thread min-sum kernels;
+// +3.5% on BP4 at p >= 0.06 once its check update took the product form --
+// the phi-sum form overflowed the instruction cache unrolled, -25%).
 
 template <int W, int T, bool BP4, int NP>
 __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, uint32_t syn_bits,
@@ -602,30 +590,19 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, u
         const uint32_t msg_s = smem_addr(msg);
 #pragma unroll 1
         for (int c = tid; c < l; c += T) {
+            // X check c and Z check l + c: both checks' loads first, then
+            // the two updates
+            constexpr int D = 2 * W;
             const int bit = c & 31;
-            // X check c (h = 0), Z check l + c (h = 1)
-            auto one = [&](int h) {
-                const int wd = h * nw + (c >> 5);
-                const uint32_t sy = gm.synw[wd] >> bit, rs = gm.resw[wd] >> bit;
-                cn_update_fixed<2 * W, BP4>(reinterpret_cast<const uint16_t *>(gm.tab + (h * l + c) * p.row_words),
-                                            msg_s, sy << 31, (rs & 1u) ? g1 : g0);
-            };
-            if constexpr (kUnrollPair<T, BP4>) {
-                // both checks' loads first, then the two updates
-                constexpr int D = 2 * W;
-                const int wd0 = c >> 5, wd1 = nw + (c >> 5);
-                const uint32_t s0 = gm.synw[wd0] >> bit, r0 = gm.resw[wd0] >> bit;
-                const uint32_t s1 = gm.synw[wd1] >> bit, r1 = gm.resw[wd1] >> bit;
-                uint32_t ad0[D], ad1[D];
-                float v0[D], v1[D];
-                cn_load<D>(reinterpret_cast<const uint16_t *>(gm.tab + c * p.row_words), msg_s, ad0, v0);
-                cn_load<D>(reinterpret_cast<const uint16_t *>(gm.tab + (l + c) * p.row_words), msg_s, ad1, v1);
-                cn_finish<D, BP4>(ad0, v0, s0 << 31, (r0 & 1u) ? g1 : g0);
-                cn_finish<D, BP4>(ad1, v1, s1 << 31, (r1 & 1u) ? g1 : g0);
-            } else {
-#pragma unroll 1
-                for (int h = 0; h < 2; ++h) one(h);
-            }
+            const int wd0 = c >> 5, wd1 = nw + (c >> 5);
+            const uint32_t s0 = gm.synw[wd0] >> bit, r0 = gm.resw[wd0] >> bit;
+            const uint32_t s1 = gm.synw[wd1] >> bit, r1 = gm.resw[wd1] >> bit;
+            uint32_t ad0[D], ad1[D];
+            float v0[D], v1[D];
+            cn_load<D>(reinterpret_cast<const uint16_t *>(gm.tab + c * p.row_words), msg_s, ad0, v0);
+            cn_load<D>(reinterpret_cast<const uint16_t *>(gm.tab + (l + c) * p.row_words), msg_s, ad1, v1);
+            cn_finish<D, BP4>(ad0, v0, s0 << 31, (r0 & 1u) ? g1 : g0);
+            cn_finish<D, BP4>(ad1, v1, s1 << 31, (r1 & 1u) ? g1 : g0);
         }
     } else {
         constexpr uint32_t kAddr = 0x00ffffffu;  // generic entries carry sym << 30
@@ -778,13 +755,8 @@ __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, i
             const int c = c0 + (tid & 31);
             uint32_t e2[2] = {0u, 0u};
             if (c < l) {
-                if constexpr (kUnrollPair<T, BP4>) {
-                    e2[0] = vn_update_fixed<W, ADD, NP>(msg + 4 * c, rowb, l0, kapc);
-                    e2[1] = vn_update_fixed<W, ADD, NP>(msg + 4 * (l + c), rowb, l0, kapc);
-                } else {
-#pragma unroll 1
-                    for (int h = 0; h < 2; ++h) e2[h] = vn_update_fixed<W, ADD, NP>(msg + 4 * (h * l + c), rowb, l0, kapc);
-                }
+                e2[0] = vn_update_fixed<W, ADD, NP>(msg + 4 * c, rowb, l0, kapc);
+                e2[1] = vn_update_fixed<W, ADD, NP>(msg + 4 * (l + c), rowb, l0, kapc);
             }
             const uint32_t eL = e2[0], eR = e2[1];
             const uint32_t xl = __ballot_sync(0xffffffffu, eL & 1u), zl = __ballot_sync(0xffffffffu, eL >> 1);
