@@ -50,7 +50,7 @@ def test_gpu_messages_vs_reference_fp64(P, cname, vn_mode, variant):
     g = P.gb_graph(P.GbSpec(*CODES[cname]))
     syn = tr[f"{cname}/syndromes"]
     cfg = _cfg(P, variant, 3, vn_mode)
-    nit = 1 if variant == "bp4" else 2
+    nit = 2
     for f in range(3):
         r = P.decode(None, g, syn[f], P.prior_llr(0.06), cfg, capture_messages=True, early_stop=False)
         for k in range(nit):

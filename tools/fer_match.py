@@ -35,12 +35,12 @@ def cfg_ns(name):
     return NS(variant=variant, l_max=100, vn_mode="marginal", alpha=alpha, gain=gain)
 
 
-def gpu(frames, out):
+def gpu(frames, out, names=NAMES):
     import paper_2605_10433_b200 as P
     g = P.gb_graph(P.GbSpec(*CODE))
     res = {}
     for p in PS:
-        for name in NAMES:
+        for name in names:
             c = cfg_ns(name)
             dcfg = P.DecoderConfig(c.variant, l_max=100, alpha=c.alpha,
                                    gain=P.GainParams(0.30, 0.50, 1.10) if c.gain else None)
@@ -50,7 +50,7 @@ def gpu(frames, out):
     np.savez_compressed(out, **res)
 
 
-def cpu(frames, gpu_npz, out, nthreads=None, fp32=True):
+def cpu(frames, gpu_npz, out, nthreads=None, fp32=True, names=NAMES):
     """fp64 oracle on the same frames; rows are written after every point so
     a long run can be inspected (and is kept) while it progresses."""
     from oracle import oracle as O
@@ -72,7 +72,7 @@ def cpu(frames, gpu_npz, out, nthreads=None, fp32=True):
 
     kw = {"nthreads": nthreads} if nthreads else {}
     for p in PS:
-        for name in NAMES:
+        for name in names:
             gf = d[f"{name}@{p}/fails"][:frames]
             git = d[f"{name}@{p}/iters"][:frames].astype(np.int64)
             of, oit, _, _ = O.frames(g, cfg_ns(name), p, p, 0, 0, frames, precision=64, **kw)
@@ -104,9 +104,10 @@ if __name__ == "__main__":
     ap.add_argument("--gpu-npz", default=os.path.join(ROOT, "gpurun_out", "fer_gpu.npz"))
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "fer_match_r01.json"))
     ap.add_argument("--threads", type=int, default=None)
+    ap.add_argument("--names", default=",".join(NAMES), help="comma-separated decoder subset")
     ap.add_argument("--no-fp32", action="store_true", help="skip the fp32-oracle equality column")
     a = ap.parse_args()
     if a.mode == "gpu":
-        gpu(a.frames, a.gpu_npz)
+        gpu(a.frames, a.gpu_npz, names=a.names.split(","))
     else:
-        cpu(a.frames, a.gpu_npz, a.out, nthreads=a.threads, fp32=not a.no_fp32)
+        cpu(a.frames, a.gpu_npz, a.out, nthreads=a.threads, fp32=not a.no_fp32, names=a.names.split(","))
