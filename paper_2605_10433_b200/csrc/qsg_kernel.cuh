@@ -647,13 +647,26 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, u
                 }
                 float C = 1.0f, Dd = 0.0f;  // suffix of edge e (edges e+1 .. d-1)
 #pragma unroll
-                for (int e = DM - 1; e >= 0; --e) {
-                    if (e < d) {
-                        const F2 t = mul2(bc(B[e]), pk(Dd, C));
-                        const float mag = fminf(fmaxf(log_ratio2(fma2(bc(A[e]), pk(C, Dd), t)), kPhi50), kPhiTiny);
-                        sts_a(ad[e], ((vs >> e) << 31) ^ f2u(mag) ^ sgn);
-                        const float Cn = fmaf(s[e], Dd, C), Dn = fmaf(s[e], C, Dd);
-                        C = Cn; Dd = Dn;
+                for (int e = DM - 1; e >= 1; e -= 2) {
+                    // edges e and e - 1: ratios, then one paired logarithm
+                    float r[2] = {1.0f, 1.0f};
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int q = e - h;
+                        if (q < d) {
+                            const F2 t = mul2(bc(B[q]), pk(Dd, C));
+                            const F2 EO = fma2(bc(A[q]), pk(C, Dd), t);
+                            r[h] = lo(EO) / hi(EO);
+                            const float Cn = fmaf(s[q], Dd, C), Dn = fmaf(s[q], C, Dd);
+                            C = Cn; Dd = Dn;
+                        }
+                    }
+                    const F2 L = log_pos2(pk(r[0], r[1]));
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int q = e - h;
+                        const float mag = fminf(fmaxf(h ? hi(L) : lo(L), kPhi50), kPhiTiny);
+                        if (q < d) sts_a(ad[q], ((vs >> q) << 31) ^ f2u(mag) ^ sgn);
                     }
                 }
             } else {

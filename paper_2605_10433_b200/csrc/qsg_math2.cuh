@@ -122,23 +122,11 @@ __device__ __forceinline__ F2 vn_F2(float y0, float y1, F2 kapc2)
     return fma2(sub2(bc(0.0f), q), log1p_01_poly2(q), log_pos2(A));
 }
 
-// log_ratio(E, O) with the two mantissa logarithms paired.
-__device__ __forceinline__ float log_ratio2(F2 EO)
-{
-    const uint32_t a = f2u(lo(EO)), b = f2u(hi(EO));
-    const float feE = u2f(kMagicBits + ((a >> 23) - 127u)) - kMagic;
-    const float feO = u2f(kMagicBits + ((b >> 23) - 127u)) - kMagic;
-    const F2 f = sub2(pk(u2f((a & 0x007fffffu) | 0x3f800000u), u2f((b & 0x007fffffu) | 0x3f800000u)), bc(1.0f));
-    const F2 r = log1p_01_2(f);
-    const float de = feE - feO;
-    return fmaf(de, kLn2Hi, fmaf(de, kLn2Lo, lo(r) - hi(r)));
-}
-
 // BP4 product-form magnitudes (qsg_math.cuh bp4_mags) for a check of
 // compile-time degree D (even): exponentials on edge pairs, the prefix and
 // suffix recurrences side by side on FFMA2 (prefix in the low half, suffix
-// in the high half), the per-edge merge as an FMUL2 + FFMA2 (E, O) pair and
-// log_ratio with its two mantissa logarithms paired.  Each half performs exactly the scalar
+// in the high half), the per-edge merge as an FMUL2 + FFMA2 (E, O) pair, the
+// ratio, and the logarithms of two edges' ratios as a pair.  Each half performs exactly the scalar
 // recipe's operations (bit-identical).
 template <int D>
 __device__ __forceinline__ void bp4_mags_fixed(const float (&x)[D], float (&mag)[D])
@@ -159,11 +147,18 @@ __device__ __forceinline__ void bp4_mags_fixed(const float (&x)[D], float (&mag)
         P = Pn; Q = Qn;
         A[j + 1] = lo(P); B[j + 1] = lo(Q); C[D - 2 - j] = hi(P); Dd[D - 2 - j] = hi(Q);
     }
+    float r[D];
 #pragma unroll
     for (int e = 0; e < D; ++e) {
         const F2 t = mul2(bc(B[e]), pk(Dd[e], C[e]));            // (B D, B C)
         const F2 EO = fma2(bc(A[e]), pk(C[e], Dd[e]), t);        // (E_e, O_e)
-        mag[e] = fminf(fmaxf(log_ratio2(EO), kPhi50), kPhiTiny);
+        r[e] = lo(EO) / hi(EO);
+    }
+#pragma unroll
+    for (int e = 0; e < D; e += 2) {
+        const F2 L = log_pos2(pk(r[e], r[e + 1]));
+        mag[e] = fminf(fmaxf(lo(L), kPhi50), kPhiTiny);
+        mag[e + 1] = fminf(fmaxf(hi(L), kPhi50), kPhiTiny);
     }
 }
 
