@@ -43,3 +43,26 @@ def test_gpu_arm_contract():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["cpu_baseline"]["value"] > 0 and d["parity"].startswith("35/35")
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+
+
+@pytest.mark.gpu
+def test_gpu_arm_two_ranks_on_one_gpu():
+    """The N > 1 code path of bench.py (sharded frames, counter all-reduce,
+    max-over-ranks timing, e2e on every rank) under torchrun with 2 ranks.
+    The pool has one GPU per box, so both ranks share it and talk over gloo
+    (QSG_BENCH_BACKEND); the N-GPU driver run uses NCCL."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, QSG_BENCH_FRAMES="16384", QSG_BENCH_BACKEND="gloo")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                          "--gpus", "2", "--steps", "1", "--warmup", "3", "--no-cpu"],
+                         capture_output=True, text=True, env=env, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["frames_per_step"] == 2 * 35 * 16384
+    assert d["e2e"]["h2d_bytes_per_step"] > 0 and "cpu_baseline" not in d
