@@ -103,12 +103,22 @@ __device__ __forceinline__ F2 log1p_01_poly2(F2 t)
 }
 __device__ __forceinline__ F2 log1p_01_2(F2 t) { return mul2(t, log1p_01_poly2(t)); }
 
-// e ln2 + log1p(m - 1) for u = 2^e m on both halves (log_pos; phi_lo's log).
+// (a & 0x7fffff) | 0x3f800000 as ONE LOP3: with both masks as immediates
+// ptxas splits it in two; the OR constant is kept in a register instead.
+__device__ __forceinline__ uint32_t mant_one(uint32_t a)
+{
+    uint32_t k, d;
+    asm volatile("mov.b32 %0, 0x3f800000;" : "=r"(k));
+    asm("lop3.b32 %0, %1, 0x007fffff, %2, 0xea;" : "=r"(d) : "r"(a), "r"(k));
+    return d;
+}
+
+// e ln2 + log1p(m - 1) for u = 2^e m on both halves (log_pos).
 __device__ __forceinline__ F2 log_pos2(F2 u)
 {
     const uint32_t a = f2u(lo(u)), b = f2u(hi(u));
     const F2 fe = sub2(pk(u2f(kMagicBits + ((a >> 23) - 127u)), u2f(kMagicBits + ((b >> 23) - 127u))), bc(kMagic));
-    const F2 f = sub2(pk(u2f((a & 0x007fffffu) | 0x3f800000u), u2f((b & 0x007fffffu) | 0x3f800000u)), bc(1.0f));
+    const F2 f = sub2(pk(u2f(mant_one(a)), u2f(mant_one(b))), bc(1.0f));
     return fma2(fe, bc(kLn2Hi), fma2(fe, bc(kLn2Lo), log1p_01_2(f)));
 }
 
