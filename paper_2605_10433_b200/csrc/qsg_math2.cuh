@@ -150,19 +150,26 @@ __device__ __forceinline__ void bp4_mags_fixed(const float (&x)[D], float (&mag)
     }
     A[0] = 1.0f; B[0] = 0.0f; C[D - 1] = 1.0f; Dd[D - 1] = 0.0f;
     F2 P = bc(1.0f), Q = bc(0.0f);  // (A_j, C_{D-1-j}), (B_j, D_{D-1-j})
+    float r[D];
+    // edge e is merged as soon as its prefix (step e - 1) and suffix (step
+    // D - 2 - e) exist, which keeps fewer partial products live
+    auto merge = [&](int e) {
+        const F2 t = mul2(bc(B[e]), pk(Dd[e], C[e]));            // (B D, B C)
+        const F2 EO = fma2(bc(A[e]), pk(C[e], Dd[e]), t);        // (E_e, O_e)
+        r[e] = lo(EO) / hi(EO);
+    };
 #pragma unroll
     for (int j = 0; j + 1 < D; ++j) {
         const F2 S = pk(s[j], s[D - 1 - j]);
         const F2 Pn = fma2(S, Q, P), Qn = fma2(S, P, Q);
         P = Pn; Q = Qn;
         A[j + 1] = lo(P); B[j + 1] = lo(Q); C[D - 2 - j] = hi(P); Dd[D - 2 - j] = hi(Q);
-    }
-    float r[D];
-#pragma unroll
-    for (int e = 0; e < D; ++e) {
-        const F2 t = mul2(bc(B[e]), pk(Dd[e], C[e]));            // (B D, B C)
-        const F2 EO = fma2(bc(A[e]), pk(C[e], Dd[e]), t);        // (E_e, O_e)
-        r[e] = lo(EO) / hi(EO);
+        // after step j: prefix known for e <= j + 1, suffix for e >= D - 2 - j
+        // (D even: the two new edges D - 2 - j and j + 1 from step D/2 - 1)
+        if (D - 2 - j < j + 1) {
+            merge(D - 2 - j);
+            merge(j + 1);
+        }
     }
 #pragma unroll
     for (int e = 0; e < D; e += 2) {
