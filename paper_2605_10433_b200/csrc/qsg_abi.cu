@@ -260,7 +260,8 @@ int compile_layout(qsg_graph *g, int32_t n, int32_t m, const int64_t *cn_ptr, co
         // ~1.1 shared-memory wavefronts per access instead of ~1.75 with the
         // row-sorted canonical order, whose position k jumps between
         // exponents across the wrap.  BP4 keeps the canonical order (its
-        // phi sum is order-dependent).
+        // prefix / suffix products round order-dependently, and the oracle
+        // multiplies in canonical order).
         const int l = g->ell, W = kind;
         std::vector<uint32_t> tab_x((size_t)mp * rw, 0);
         for (int i = 0; i < m; ++i) {

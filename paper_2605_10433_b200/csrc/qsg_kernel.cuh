@@ -24,7 +24,8 @@
 // so rows start in distinct banks) u32 words per check: generic rows hold
 // byte offsets (+ the edge symbol) in canonical order and an info word at
 // index dc_max; bicycle rows hold u16 slot indices, in canonical order for
-// BP4 (the order of its phi sum) and in exponent order for the order-free
+// BP4 (the order of its prefix / suffix products) and in exponent order for
+// the order-free
 // min-sum update (consecutive checks -> consecutive qubits, few bank
 // conflicts).  Generic kernels keep hard decisions as one u32 per qubit.
 //

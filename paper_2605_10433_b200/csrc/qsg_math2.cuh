@@ -4,8 +4,9 @@
 // independent IEEE binary32 fused multiply-adds / adds / multiplies, each
 // rounded exactly like its scalar counterpart.  The kernels spend most of
 // their issue slots on these recipes, and they always evaluate them on
-// independent pairs (the two factors F(S_Z), F(S_X) of a qubit, the phi of
-// edges k and k+1 of a check), so every function below is the scalar recipe
+// independent pairs (the two factors F(S_Z), F(S_X) of a qubit; the
+// exponentials, prefix / suffix steps and logarithms of a BP4 check), so
+// every function below is the scalar recipe
 // applied to both halves of an F2, operation for operation: the results are
 // bit-identical to two calls of the scalar version (and therefore to the
 // oracle).  Integer / bit manipulations and selects run per half; there is
