@@ -25,9 +25,8 @@
 // byte offsets (+ the edge symbol) in canonical order and an info word at
 // index dc_max; bicycle rows hold u16 slot indices, in canonical order for
 // BP4 (the order of its prefix / suffix products) and in exponent order for
-// the order-free
-// min-sum update (consecutive checks -> consecutive qubits, few bank
-// conflicts).  Generic kernels keep hard decisions as one u32 per qubit.
+// the order-free min-sum update (consecutive checks -> consecutive qubits,
+// few bank conflicts).  Generic kernels keep hard decisions as one u32 per qubit.
 //
 // The fp32 recipes (qsg_math.cuh) run scalar or, where two independent
 // evaluations exist, paired on FFMA2 / FADD2 / FMUL2 (qsg_math2.cuh) with
