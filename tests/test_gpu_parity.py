@@ -274,3 +274,31 @@ def test_paired_recipes_equal_scalar_on_device(tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert "RECIPE_MISMATCHES 0" in out.stdout, out.stdout[-2000:]
     assert out.returncode == 0
+
+
+@pytest.mark.parametrize("variant,kw", CFGS)
+def test_edge_cases_match_oracle(P, oracle, variant, kw):
+    """Empty batches, an error-free channel (epsilon = 0: all-I errors, zero
+    syndromes, success at iteration 1 with e_hat = I), l_max = 1 (no message
+    update at all: decoder.py:454-460) and an all-zero syndrome batch, on
+    the bicycle and the generic kernels, against the oracle."""
+    for spec in (GB254, SMALL):
+        g = P.gb_graph(P.GbSpec(*spec))
+        cfg = _cfg(P, variant, kw, l_max=20)
+        # empty inputs
+        r = P.decode_batch(g, np.zeros((0, g.m), np.uint8), P.prior_llr(0.05), cfg)
+        assert r.success.shape == (0,) and r.e_hat.shape == (0, g.n) and r.iterations.shape == (0,)
+        f, it = P.decode_frames(g, cfg, 0.05, 0.05, 0, 0, 0)
+        assert f.shape == (0,) and it.shape == (0,)
+        # epsilon = 0: every frame decodes at iteration 1 (matched eps0 > 0)
+        f, it = P.decode_frames(g, cfg, 0.0, 0.05, 3, 0, 257)
+        assert not f.any() and (it == 1).all()
+        # l_max = 1 on noisy frames: success iff the syndrome is zero
+        one = _cfg(P, variant, kw, l_max=1)
+        f, it, eh = P.decode_frames_device(g, one, 0.03, 0.03, 7, 0, 300, want_ehat=True)
+        of, oi, oe, _ = oracle.frames(g, one, 0.03, 0.03, 7, 0, 300, want_ehat=True)
+        assert np.array_equal(f.cpu().numpy().astype(bool), of) and np.array_equal(it.cpu().numpy(), oi)
+        assert np.array_equal(eh.cpu().numpy(), oe)
+        # all-zero syndromes: success at iteration 1, e_hat all I
+        r = P.decode_batch(g, np.zeros((33, g.m), np.uint8), P.prior_llr(0.05), cfg)
+        assert r.success.all() and (r.iterations == 1).all() and not r.e_hat.any()
