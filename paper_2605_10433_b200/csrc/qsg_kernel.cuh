@@ -649,24 +649,22 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, u
 #pragma unroll
                 for (int e = DM - 1; e >= 1; e -= 2) {
                     // edges e and e - 1: ratios, then one paired logarithm
-                    float r[2] = {1.0f, 1.0f};
+                    F2 eo[2] = {bc(1.0f), bc(1.0f)};
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int q = e - h;
                         if (q < d) {
                             const F2 t = mul2(bc(B[q]), pk(Dd, C));
-                            const F2 EO = fma2(bc(A[q]), pk(C, Dd), t);
-                            r[h] = lo(EO) / hi(EO);
+                            eo[h] = fma2(bc(A[q]), pk(C, Dd), t);
                             const float Cn = fmaf(s[q], Dd, C), Dn = fmaf(s[q], C, Dd);
                             C = Cn; Dd = Dn;
                         }
                     }
-                    const F2 L = log_pos2(pk(r[0], r[1]));
+                    const F2 m = bp4_out2(eo[0], eo[1]);
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int q = e - h;
-                        const float mag = fminf(fmaxf(h ? hi(L) : lo(L), kPhi50), kPhiTiny);
-                        if (q < d) sts_a(ad[q], ((vs >> q) << 31) ^ f2u(mag) ^ sgn);
+                        if (q < d) sts_a(ad[q], ((vs >> q) << 31) ^ f2u(h ? hi(m) : lo(m)) ^ sgn);
                     }
                 }
             } else {

@@ -133,11 +133,29 @@ __device__ __forceinline__ F2 vn_F2(float y0, float y1, F2 kapc2)
     return fma2(sub2(bc(0.0f), q), log1p_01_poly2(q), log_pos2(A));
 }
 
+// rcp3 on both halves (o > 0).
+__device__ __forceinline__ F2 rcp3_2(F2 o)
+{
+    F2 y = pk(u2f(0x7ef311c3u - f2u(lo(o))), u2f(0x7ef311c3u - f2u(hi(o))));
+    const F2 no = sub2(bc(0.0f), o);  // -o, exact
+#pragma unroll
+    for (int i = 0; i < 3; ++i) y = fma2(y, fma2(no, y, bc(1.0f)), y);
+    return y;
+}
+
+// BP4 magnitudes of two edges from their (E, O) pairs.
+__device__ __forceinline__ F2 bp4_out2(F2 EOa, F2 EOb)
+{
+    const F2 y = rcp3_2(pk(fmaxf(hi(EOa), 1e-30f), fmaxf(hi(EOb), 1e-30f)));
+    const F2 L = log_pos2(mul2(pk(lo(EOa), lo(EOb)), y));
+    return pk(fminf(fmaxf(lo(L), kPhi50), kPhiTiny), fminf(fmaxf(hi(L), kPhi50), kPhiTiny));
+}
+
 // BP4 product-form magnitudes (qsg_math.cuh bp4_mags) for a check of
 // compile-time degree D (even): exponentials on edge pairs, the prefix and
 // suffix recurrences side by side on FFMA2 (prefix in the low half, suffix
-// in the high half), the per-edge merge as an FMUL2 + FFMA2 (E, O) pair, the
-// ratio, and the logarithms of two edges' ratios as a pair.  Each half performs exactly the scalar
+// in the high half), the per-edge merge as an FMUL2 + FFMA2 (E, O) pair, and
+// the reciprocal, ratio and logarithm of two edges as pairs.  Each half performs exactly the scalar
 // recipe's operations (bit-identical).
 template <int D>
 __device__ __forceinline__ void bp4_mags_fixed(const float (&x)[D], float (&mag)[D])
@@ -151,13 +169,12 @@ __device__ __forceinline__ void bp4_mags_fixed(const float (&x)[D], float (&mag)
     }
     A[0] = 1.0f; B[0] = 0.0f; C[D - 1] = 1.0f; Dd[D - 1] = 0.0f;
     F2 P = bc(1.0f), Q = bc(0.0f);  // (A_j, C_{D-1-j}), (B_j, D_{D-1-j})
-    float r[D];
-    // edge e is merged as soon as its prefix (step e - 1) and suffix (step
-    // D - 2 - e) exist, which keeps fewer partial products live
+    // edges are merged as soon as their prefix (step e - 1) and suffix
+    // (step D - 2 - e) exist -- two per step from step D/2 - 1, which keeps
+    // fewer partial products live -- and finished as a pair
     auto merge = [&](int e) {
         const F2 t = mul2(bc(B[e]), pk(Dd[e], C[e]));            // (B D, B C)
-        const F2 EO = fma2(bc(A[e]), pk(C[e], Dd[e]), t);        // (E_e, O_e)
-        r[e] = lo(EO) / hi(EO);
+        return fma2(bc(A[e]), pk(C[e], Dd[e]), t);               // (E_e, O_e)
     };
 #pragma unroll
     for (int j = 0; j + 1 < D; ++j) {
@@ -165,18 +182,11 @@ __device__ __forceinline__ void bp4_mags_fixed(const float (&x)[D], float (&mag)
         const F2 Pn = fma2(S, Q, P), Qn = fma2(S, P, Q);
         P = Pn; Q = Qn;
         A[j + 1] = lo(P); B[j + 1] = lo(Q); C[D - 2 - j] = hi(P); Dd[D - 2 - j] = hi(Q);
-        // after step j: prefix known for e <= j + 1, suffix for e >= D - 2 - j
-        // (D even: the two new edges D - 2 - j and j + 1 from step D/2 - 1)
-        if (D - 2 - j < j + 1) {
-            merge(D - 2 - j);
-            merge(j + 1);
+        if (D - 2 - j < j + 1) {  // new edges D - 2 - j and j + 1
+            const F2 m = bp4_out2(merge(D - 2 - j), merge(j + 1));
+            mag[D - 2 - j] = lo(m);
+            mag[j + 1] = hi(m);
         }
-    }
-#pragma unroll
-    for (int e = 0; e < D; e += 2) {
-        const F2 L = log_pos2(pk(r[e], r[e + 1]));
-        mag[e] = fminf(fmaxf(lo(L), kPhi50), kPhiTiny);
-        mag[e + 1] = fminf(fmaxf(hi(L), kPhi50), kPhiTiny);
     }
 }
 

@@ -21,7 +21,7 @@ __global__ void k(const float* x, float* o, int n, int which) {
     case 1: s0 = log1p_01(a); s1 = log1p_01(b); r = log1p_01_2(pk(a, b)); break;
     case 2: s0 = log_pos(a); s1 = log_pos(b); r = log_pos2(pk(a, b)); break;
     case 3: s0 = vn_F(a, 0.03f); s1 = vn_F(b, 0.03f); r = vn_F2(a, b, bc(0.03f)); break;
-    case 4: s0 = log_pos(a / b); s1 = log_pos(b / a); r = log_pos2(pk(a / b, b / a)); break;
+    case 4: s0 = rcp3(a); s1 = rcp3(b); r = rcp3_2(pk(a, b)); break;
     case 5: case 6: case 7: {  // one BP4 check (degree 10 / 10 / 6) from (a, b)
       float x[10], ms[10], mp[10];
       for (int q = 0; q < 10; ++q) x[q] = fminf(fabsf(a * (1.0f + q) - b * (3.0f - 0.7f * q)), 64.0f);
@@ -60,7 +60,7 @@ int main() {
   const int n = 1 << 20;
   float *h = new float[n], *ho = new float[2 * n];
   float *d, *dout; cudaMalloc(&d, n * 4); cudaMalloc(&dout, 2 * n * 4);
-  const char* names[] = {"exp_neg", "log1p_01", "log_pos", "vn_F", "log_pos_ratio", "bp4_d10_ends", "bp4_d10_mid", "bp4_d6", "sub_add", "fma_imm", "mul", "add", "subc", "sub_add2"};
+  const char* names[] = {"exp_neg", "log1p_01", "log_pos", "vn_F", "rcp3", "bp4_d10_ends", "bp4_d10_mid", "bp4_d6", "sub_add", "fma_imm", "mul", "add", "subc", "sub_add2"};
   int recipe_bad = 0;
   for (int w = 0; w < 14; ++w) {
     srand(1);
