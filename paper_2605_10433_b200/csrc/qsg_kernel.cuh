@@ -404,21 +404,36 @@ __device__ __forceinline__ int circ_syndrome(const KParams &p, const GroupMem &g
 }
 
 // The same syndrome with every loop-invariant part hoisted: a thread's word
-// w, its 32-bit windows (bitmap word, shift, wrap) and the word's valid mask
-// depend only on its lane and the code, so they are computed once per
-// kernel.  Window descriptor: bits 0-9 word index of B[q] in gm.bits,
-// 10-19 word index of B[0] of that bitmap, 20-24 shift, 25-29 wrap shift
-// n1 = l - start (0: no wrap), 31 valid.  Needs lpw >= 4 (at most
-// ceil(2W / 4) windows per lane; the host guarantees it for every bicycle
-// shape it builds, else circ_syndrome is used).
+// w, its 32-bit windows and the word's valid mask depend only on its lane
+// and the code, so they are computed once per kernel, as shared-window byte
+// addresses: lo[j] = address of B[q] | shift << 24, hi[j] = address of B[0]
+// of that bitmap | wrap << 24, wrap = l - start when the window wraps, else
+// 32 (PTX shl by >= 32 gives 0).  Unused windows point at a bitmap's zero
+// padding word with shift 0 and wrap 32, so every window is evaluated
+// without a branch.  Needs lpw >= 4 (at most ceil(2W / 4) windows per lane;
+// the host guarantees it for every bicycle shape it builds, else
+// circ_syndrome is used).
 template <int W>
 struct SynPlan {
     static constexpr int K = (2 * W + 3) / 4;
-    uint32_t d[K];
+    uint32_t lo[K], hi[K];
     uint32_t mask;  // valid bits of word w (0 for idle lanes)
     int w;          // syndrome word (X words then Z words), -1 idle
     bool writer;    // first lane of its word
 };
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a)
+{
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t shl_clamp(uint32_t x, uint32_t n)  // x << n, 0 for n >= 32
+{
+    uint32_t d;
+    asm("shl.b32 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(n));
+    return d;
+}
 
 template <int W, int T>
 __device__ __forceinline__ SynPlan<W> syn_plan(const KParams &p, const GroupMem &gm, int tid)
@@ -426,9 +441,14 @@ __device__ __forceinline__ SynPlan<W> syn_plan(const KParams &p, const GroupMem 
     SynPlan<W> P;
     const int nw = p.nw, l = p.ell, lpw = p.lpw;
     const int w = tid / lpw, sub = tid - w * lpw;
+    const uint32_t bits_s = smem_addr(gm.bits);
+    const uint32_t zero = bits_s + 4u * (uint32_t)nw;  // XL padding word (always 0)
     P.w = -1; P.mask = 0u; P.writer = false;
 #pragma unroll
-    for (int j = 0; j < SynPlan<W>::K; ++j) P.d[j] = 0u;
+    for (int j = 0; j < SynPlan<W>::K; ++j) {
+        P.lo[j] = zero;
+        P.hi[j] = zero | (32u << 24);
+    }
     if (w < 2 * nw) {
         const bool zc = w >= nw;
         const int ww = zc ? w - nw : w;
@@ -446,10 +466,10 @@ __device__ __forceinline__ SynPlan<W> syn_plan(const KParams &p, const GroupMem 
                 start = start >= l ? start - l : start;
                 start = start >= l ? start - l : start;
                 const int blk = left ? (zc ? kXL : kZL) : (zc ? kXR : kZR);
-                const uint32_t b0 = (uint32_t)(blk * (nw + 1));
+                const uint32_t b0 = bits_s + 4u * (uint32_t)(blk * (nw + 1));
                 const uint32_t n1 = (uint32_t)(l - start);
-                P.d[j] = (b0 + (uint32_t)(start >> 5)) | (b0 << 10) | ((uint32_t)(start & 31) << 20) |
-                         ((n1 < 32u ? n1 : 0u) << 25) | 0x80000000u;
+                P.lo[j] = (b0 + 4u * (uint32_t)(start >> 5)) | ((uint32_t)(start & 31) << 24);
+                P.hi[j] = b0 | ((n1 < 32u ? n1 : 32u) << 24);
             }
         }
     }
@@ -463,14 +483,10 @@ __device__ __forceinline__ int circ_syndrome_plan(const SynPlan<W> &P, const Gro
     uint32_t acc = 0;
 #pragma unroll
     for (int j = 0; j < SynPlan<W>::K; ++j) {
-        const uint32_t d = P.d[j];
-        if (d & 0x80000000u) {
-            const uint32_t *B = gm.bits + (d & 0x3ffu);
-            uint32_t x = __funnelshift_r(B[0], B[1], d >> 20);
-            const uint32_t n1 = (d >> 25) & 31u;
-            if (n1) x |= gm.bits[(d >> 10) & 0x3ffu] << n1;
-            acc ^= x;
-        }
+        const uint32_t a = P.lo[j] & 0x00ffffffu, b = P.hi[j] & 0x00ffffffu;
+        uint32_t x = __funnelshift_r(lds_u32(a), lds_u32(a + 4u), P.lo[j] >> 24);
+        x |= shl_clamp(lds_u32(b), P.hi[j] >> 24);
+        acc ^= x;
     }
     acc ^= __shfl_xor_sync(0xffffffffu, acc, 1);
     acc ^= __shfl_xor_sync(0xffffffffu, acc, 2);
