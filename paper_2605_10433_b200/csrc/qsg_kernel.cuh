@@ -990,7 +990,8 @@ __global__ void __launch_bounds__(640) decode_kernel(const KParams p)
                 group_sync<T>(g);
                 bitmaps_from_bytes<T>(p, gm, eb, tid);
                 group_sync<T>(g);
-                circ_syndrome<W, T>(p, gm, nullptr, gm.synw, tid);
+                if (use_plan) circ_syndrome_plan<W, T>(plan, gm, nullptr, gm.synw, p.lpw);
+                else circ_syndrome<W, T>(p, gm, nullptr, gm.synw, tid);
                 group_sync<T>(g);  // every warp done reading the bitmaps before they are reset below
             } else if (p.syn_words) {
                 // bit-packed rows: X checks are bits [0, l), Z checks [l, 2l)
