@@ -424,6 +424,16 @@ void fill_cfg_params(const qsg_decoder_cfg *c, double l0, qsg::KParams &p)
     p.v0 = (float)v0;
     p.alpha = (float)c->alpha;
     p.amin = c->alpha_min; p.amax = c->alpha_max; p.eta = c->eta_unsat;
+    // first check update in closed form (decode_kernel, cn_phase_first):
+    // bicycle kernels with v0 > 0; BP4 magnitudes by the shared recipe
+    p.first_fast = (p.ell > 0 && p.v0 > 0.0f) ? 1 : 0;
+    if (p.first_fast && c->variant == QSG_BP4) {
+        const int D = p.dv_max;  // bicycle: every check and qubit has degree 2W
+        float x[16], mag[16];
+        for (int k = 0; k < D; ++k) x[k] = std::min(p.v0, 64.0f);
+        qsg::bp4_mags(x, D, mag);
+        for (int k = 0; k < D; ++k) p.first_bp4[k] = qsg::f2u(mag[k]);
+    }
     // SAGMS gains per unsat count (decoder.py:464-465), the kernel's double
     // recipe evaluated here once instead of a double division per iteration
     // and frame; volatile keeps each product rounded (no contraction)

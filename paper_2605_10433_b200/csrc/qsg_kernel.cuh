@@ -71,6 +71,8 @@ struct KParams {
     float l0, v0, alpha;
     float kapc;  // e^-l0 (vn_F)
     double amin, amax, eta;
+    int32_t first_fast;         // bicycle kernels, v0 > 0: first check update from the values below
+    uint32_t first_bp4[16];     // BP4: the first update's output bits at row position k (v0 inputs, sign +)
     int32_t use_gtab;           // SAGMS: gains from gtab (host double, decoder.py:464-465) when m < kGainTab
     float gtab[2 * kGainTab];   // gtab[2u] = (float)base(u), gtab[2u+1] = (float)(base(u) * eta), u = unsat
     // input
@@ -596,6 +598,43 @@ __device__ __forceinline__ void cn_finish(const uint32_t (&ad)[D], const float (
 // +3.5% on BP4 at p >= 0.06 once its check update took the product form --
 // the phi-sum form overflowed the instruction cache unrolled, -25%).
 
+// First iteration (decoder.py:405-410): every qubit->check message is v0,
+// so every check sees D equal inputs and its update is known in closed form:
+// min-sum sends sign(s_i) gain_i min(v0, 64) on every edge (min1 = min2 =
+// v0, sign product +), BP4 sends the product-form magnitude of D copies of
+// min(v0, 64) at row position k (host-computed with the same recipe,
+// KParams::first_bp4) with sign(s_i).  These are the words the general
+// update stores (the -m gpu parity suite checks every frame bit for bit);
+// the check phase of iteration 1 then costs a table load and a store per
+// edge.  Needs v0 > 0 (then the hard decision of iteration 1 is I and the
+// residual equals the syndrome).
+template <int W, int T, bool BP4>
+__device__ __forceinline__ void cn_phase_first(const KParams &p, const GroupMem &gm, float g0, float g1, int tid)
+{
+    constexpr int D = 2 * W;
+    const int l = p.ell, nw = p.nw;
+    const uint32_t msg_s = smem_addr(gm.msg);
+    const float a = fminf(p.v0, kClip);
+    const uint32_t m0 = f2u(fminf(g0 * a, kClip)), m1 = f2u(fminf(g1 * a, kClip));
+#pragma unroll 1
+    for (int c = tid; c < l; c += T) {
+        const int bit = c & 31;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int wd = h * nw + (c >> 5);
+            const uint32_t s = (gm.synw[wd] >> bit) & 1u, r = (gm.resw[wd] >> bit) & 1u;
+            const uint16_t *row = reinterpret_cast<const uint16_t *>(gm.tab + (h * l + c) * p.row_words);
+            const uint32_t sg = s << 31;
+            const uint32_t ms = (r ? m1 : m0) ^ sg;
+#pragma unroll
+            for (int q = 0; q < D; ++q) {
+                const uint32_t w = BP4 ? (p.first_bp4[q] ^ sg) : ms;
+                sts_a(msg_s + 4u * lds_u16(row + q), w);
+            }
+        }
+    }
+}
+
 template <int W, int T, bool BP4, int NP>
 __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, uint32_t syn_bits,
                                          uint32_t res_bits, float g0, float g1, int tid)
@@ -1097,7 +1136,10 @@ __global__ void __launch_bounds__(640) decode_kernel(const KParams p)
                     g1 = (float)(base * p.eta);
                 }
             }
-            cn_phase<W, T, BP4, NP>(p, gm, syn_bits, res, g0, g1, tid);
+            if (W > 0 && ell == 1 && p.first_fast)
+                cn_phase_first<(W > 0 ? W : 1), T, BP4>(p, gm, g0, g1, tid);
+            else
+                cn_phase<W, T, BP4, NP>(p, gm, syn_bits, res, g0, g1, tid);
             group_sync<T>(g);
             if (capture && p.tr_cn) snapshot<T>(p, gm.msg, p.tr_cn + (f * p.l_max + n_snap) * p.E, tid, false);
             vn_phase<W, T, BP4, ADD, NP>(p, gm, tid);
