@@ -1090,8 +1090,12 @@ __global__ void __launch_bounds__(640) decode_kernel(const KParams p)
             }
             for (int j = tid; j < np_; j += T) gm.ehat[j] = hd0;
         }
-        const uint32_t v0b = f2u(p.v0);
-        for (int s = tid; s < msg_words; s += T) sts_u(gm.msg, 4u * s, v0b);
+        // the initial qubit->check messages (v0); not needed when the first
+        // check update is the closed form, which writes every edge slot
+        if (!(W > 0 && p.first_fast)) {
+            const uint32_t v0b = f2u(p.v0);
+            for (int s = tid; s < msg_words; s += T) sts_u(gm.msg, 4u * s, v0b);
+        }
         group_sync<T>(g);
 
         int recorded = 0, success = 0, iters = p.l_max, n_gamma = 0, n_snap = 0;
