@@ -302,3 +302,11 @@ def test_edge_cases_match_oracle(P, oracle, variant, kw):
         # all-zero syndromes: success at iteration 1, e_hat all I
         r = P.decode_batch(g, np.zeros((33, g.m), np.uint8), P.prior_llr(0.05), cfg)
         assert r.success.all() and (r.iterations == 1).all() and not r.e_hat.any()
+        # mismatched priors around eps0 = 3/4, where v0 (and L0) change sign:
+        # the closed-form first check update (v0 > 0) and the general one
+        short = _cfg(P, variant, kw, l_max=6)
+        for eps0 in (0.70, 0.749, 0.76, 0.9):
+            f, it, eh = P.decode_frames_device(g, short, 0.05, eps0, 11, 0, 200, want_ehat=True)
+            of, oi, oe, _ = oracle.frames(g, short, 0.05, eps0, 11, 0, 200, want_ehat=True)
+            assert np.array_equal(f.cpu().numpy().astype(bool), of), eps0
+            assert np.array_equal(it.cpu().numpy(), oi) and np.array_equal(eh.cpu().numpy(), oe), eps0
