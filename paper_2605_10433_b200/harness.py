@@ -246,16 +246,16 @@ def run_point(graph, cfg: SweepConfig, epsilon: float, batch_frames: int = GPU_B
     batches = frame_batches(graph, cfg.decoder, epsilon, eps0, cfg.seed, cfg.max_frames, batch_frames)
     for fails, iters in batches:
         count = len(fails)
-        cum = np.cumsum(fails)
-        hit = np.nonzero(failures + cum >= cfg.target_failures)[0]
-        if hit.size:
-            stop = int(hit[0]) + 1
+        nfail = int(np.count_nonzero(fails))
+        if failures + nfail >= cfg.target_failures:  # the stop frame is in this batch
+            cum = np.cumsum(fails)
+            stop = int(np.nonzero(failures + cum >= cfg.target_failures)[0][0]) + 1
             frames = start + stop
             failures += int(cum[stop - 1])
             iter_sum += int(iters[:stop].sum())
             break
         frames = start + count
-        failures += int(cum[-1]) if count else 0
+        failures += nfail
         iter_sum += int(iters.sum())
         start += count
     batches.close()
