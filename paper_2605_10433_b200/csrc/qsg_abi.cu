@@ -426,7 +426,7 @@ void fill_cfg_params(const qsg_decoder_cfg *c, double l0, qsg::KParams &p)
     p.amin = c->alpha_min; p.amax = c->alpha_max; p.eta = c->eta_unsat;
     // first check update in closed form (decode_kernel, cn_phase_first):
     // bicycle kernels with v0 > 0; BP4 magnitudes by the shared recipe
-    p.first_fast = (p.ell > 0 && p.v0 > 0.0f) ? 1 : 0;
+    p.first_fast = (p.ell > 0 && p.v0 > 0.0f && p.dv_max <= 16) ? 1 : 0;  // bicycle: D = 2W <= 16
     if (p.first_fast && c->variant == QSG_BP4) {
         const int D = p.dv_max;  // bicycle: every check and qubit has degree 2W
         float x[16], mag[16];
