@@ -14,6 +14,18 @@ summed over ranks with one NCCL all-reduce per point.
 --impl reference times the CPU oracle port (oracle/, the reference's
 algorithm restated in C, all host threads) on a bounded sample of the same
 workload (the first frames of every point).
+
+Every run also measures the north-star scaling workload, BASELINE configs[4]
+(`strong_config5` in the JSON line): [[254,28]] and the random l=511 w=5 GB
+code, SAGMS, p in {0.03, 0.08}, l_max 100, a FIXED 2^22 frames per point
+sharded contiguously over the N ranks (strong scaling), the four points
+launched back to back with ONE all-reduce of the counter block at the end
+and no host synchronisation in between.
+
+With --gpus N > 1 and no torchrun environment (WORLD_SIZE unset) the script
+re-executes itself under torch.distributed.run with N local ranks
+(rendezvous on 127.0.0.1).  NCCL's init log (NCCL_DEBUG=INFO,
+NCCL_DEBUG_SUBSYS=INIT unless set) records the communicator's rank count.
 """
 from __future__ import annotations
 
@@ -40,6 +52,12 @@ METRIC = "decoded frames/s and CN-edge updates/s per GPU & 8×B200 (% roofline),
 # Algorithmic ops per CN-edge update: ALU + MUFU-class
 # ops of the reference algorithm, the numerator of roofline.achieved.
 OPS_PER_EDGE = {"sagms": 30.3 + 4, "sms": 30.0 + 4, "ms": 29.0 + 4, "bp4": 34.1 + 10}
+
+
+# BASELINE configs[4] (strong scaling): GbSpec args, p values, total frames per point
+C5_CODES = (("[[254,28]]", CODE), ("l511w5", (511, (0, 5, 200, 397, 418), (0, 81, 284, 347, 418))))
+C5_PS = (0.03, 0.08)
+C5_FRAMES = int(os.environ.get("QSG_BENCH_C5_FRAMES", 1 << 22))  # override: tests only
 
 
 def decoders(P):
@@ -315,6 +333,7 @@ def run_ours(args, rank, world, local_rank):
     if world == 1:
         assert int(h_out[:, 8 * FRAMES_PER_POINT:].sum()) == int(cnt[:, 0].sum() - cnt[:, 1].sum())
 
+    c5 = strong_config5(args, rank, world, dev, l2)
     if rank != 0:
         return
     # ---- roofline of the dominant kernel (min-sum marginal, bicycle W=5) ----
@@ -400,6 +419,7 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clocks,
         "fer": fer,
     }
+    line["strong_config5"] = c5
     if cpu:
         line["cpu_baseline"] = cpu
     if parity:
@@ -407,9 +427,105 @@ def run_ours(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def strong_config5(args, rank, world, dev, l2):
+    """BASELINE configs[4]: a fixed 2^22 frames per point, sharded over the
+    ranks; all four points back to back, one all-reduce, max over ranks.
+    On one GPU also a proxy of the 8-GPU step: each of the 8 shards of every
+    point timed alone (CUDA events), the step of the slowest shard summed over
+    the points -> t(2^22) / (8 x max-shard time)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_10433_b200 as P
+    from paper_2605_10433_b200.dist import shard_range
+    cfg = P.DecoderConfig("sagms", l_max=L_MAX, gain=P.GainParams(0.30, 0.50, 1.10))
+    pts = []
+    for cname, spec in C5_CODES:
+        dg = P.device_graph(P.gb_graph(P.GbSpec(*spec)), dev)
+        for p in C5_PS:
+            pts.append((cname, dg, p))
+    lo, n = shard_range(rank, world, 0, C5_FRAMES)
+    cnt = torch.zeros((len(pts), 4), dtype=torch.int64, device=dev)
+
+    def step():
+        cnt.zero_()
+        for k, (_, dg, p) in enumerate(pts):
+            P.decode_frames_device(dg, cfg, p, p, SEED, lo, n, counters=cnt[k], want_frames=False)
+        if world > 1:
+            dist.all_reduce(cnt)
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    times = []
+    for _ in range(args.steps):
+        flush_l2(l2)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        step()
+        b.record()
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b))
+    t = torch.tensor(times, dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.mean())
+    c = cnt.cpu().numpy()
+    frames = int(c[:, 0].sum())
+    out = {"value": frames / (ms / 1e3), "unit": "frames/s", "scaling": "strong", "n_gpus": world,
+           "ms_per_step": ms, "frames_per_step": frames,
+           "cn_edge_updates_per_s": float(c[:, 3].sum()) / (ms / 1e3),
+           "workload": "configs[4]: [[254,28]] + random GB l=511 w=5 (seed 0), SAGMS(0.30,0.50,1.10), "
+                       "p in {0.03,0.08}, l_max 100, 2^22 frames/point in total sharded over the ranks, "
+                       "4 points back to back + one NCCL all-reduce per step, max over ranks",
+           "points": [{"code": cname, "p": p, "frames": int(c[k, 0]), "failures": int(c[k, 1]),
+                       "fer": float(c[k, 1] / max(1, c[k, 0])), "mean_iterations": float(c[k, 2] / max(1, c[k, 0]))}
+                      for k, (cname, _, p) in enumerate(pts)]}
+    if world == 1:
+        # one-GPU proxy of the 8-way split: shard r of 8 of every point alone
+        shard_ms = [[0.0] * len(pts) for _ in range(8)]
+        for rep in range(2):  # first pass warms each shard's launch
+            for r in range(8):
+                slo, sn = shard_range(r, 8, 0, C5_FRAMES)
+                for k, (_, dg, p) in enumerate(pts):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    P.decode_frames_device(dg, cfg, p, p, SEED, slo, sn, counters=None, want_frames=False)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    if rep:
+                        shard_ms[r][k] = e0.elapsed_time(e1)
+        per_rank = [sum(x) for x in shard_ms]
+        out["proxy_8way"] = {
+            "shard_ms_max_over_8": max(per_rank), "shard_ms_min_over_8": min(per_rank),
+            "efficiency": ms / (8 * max(per_rank)),
+            "note": "t(2^22 frames on 1 GPU) / (8 x slowest 1/8 shard timed alone): the strong-scaling "
+                    "efficiency an 8-GPU run would reach with zero collective cost"}
+    return out
+
+
 def dg_sms():
     import torch
     return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+
+
+def spawn(n):
+    """Re-execute this script under torch.distributed.run with n local ranks
+    (one process per GPU), rendezvous on 127.0.0.1 at a free port."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execve(sys.executable, cmd, env)
 
 
 def main():
@@ -422,6 +538,8 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn(args.gpus)  # does not return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -435,6 +553,8 @@ def main():
         torch.cuda.set_device(dev_index)
         # QSG_BENCH_BACKEND=gloo exercises the multi-rank logic on one GPU
         backend = os.environ.get("QSG_BENCH_BACKEND", "nccl")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init log: nranks visible
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
         else:

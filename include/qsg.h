@@ -95,6 +95,14 @@ int qsg_graph_info(const qsg_graph *g, int32_t *n, int32_t *m, int64_t *E, int32
 int qsg_graph_export(const qsg_graph *g, int64_t *edge_cn, int64_t *edge_vn, uint8_t *edge_sym,
                      int64_t *cn_ptr, int64_t *vn_order, int64_t *vn_ptr);
 
+/* Row commutation of the check matrix on the graph's device (the
+ * stabilizer validation of SparseCheckMatrix.validate, code.py:80-97, via
+ * pauli.check_orthogonality, pauli.py:120-144), in O(m d_c d_v d_c) rather
+ * than the reference's O(m^2) pair scan.  Synchronous (setup-time call).
+ * *commutes = 1 iff every pair of rows commutes; bad_pair (int64[2], may be
+ * NULL) receives the lowest anticommuting pair (i, k), i < k, or (-1, -1). */
+int qsg_graph_check_commute(const qsg_graph *g, int32_t *commutes, int64_t *bad_pair);
+
 /* Optional per-frame traces of qsg_decode_syndromes (device buffers, any may
  * be NULL):
  *   unsat[B * l_max]         residual weight per executed iteration

@@ -24,7 +24,9 @@ from .codes import (  # noqa: E402
     CodeGraph,
     GbSpec,
     as_code_graph,
+    OrthogonalityError,
     check_commute,
+    check_commute_device,
     code_dimension,
     csr_graph,
     gb_dimension,
@@ -63,19 +65,20 @@ from .harness import (  # noqa: E402
     wilson_interval,
 )
 
-# reference spelling of the graph builders
+# reference spelling of the graph builders and code I/O
 build_gb_graph = gb_graph
 tanner_graph = as_code_graph
+load_code = load_qpc
 
 __all__ = [
     "__version__", "ChannelPrior", "DepolarizingChannel", "prior_llr", "sample_error",
     "sample_errors", "sample_errors_device", "CodeFormatError", "CodeGraph", "GbSpec",
-    "as_code_graph", "check_commute", "code_dimension", "csr_graph", "gb_dimension", "gb_graph",
+    "as_code_graph", "check_commute", "check_commute_device", "OrthogonalityError", "code_dimension", "csr_graph", "gb_dimension", "gb_graph",
     "load_qpc", "random_gb_spec", "save_qpc", "BatchDecodeResult", "DecodeResult",
     "DecoderConfig", "EdgeMessageState", "GainParams", "decode", "decode_batch",
     "decode_batch_device", "decode_batch_packed", "decode_batch_packed_device", "pack_syndromes",
     "effective_gain", "syndrome_ratio", "DeviceGraph", "device_graph",
     "FerPoint", "SweepConfig", "config_digest", "decode_frames", "decode_frames_device",
     "install", "run_point", "run_sweep", "wilson_interval", "build_gb_graph", "tanner_graph",
-    "HostBatch", "decode_host_batches",
+    "HostBatch", "decode_host_batches", "load_code",
 ]

@@ -28,7 +28,7 @@ EXPORTS = (
     "qsg_graph_create_gb", "qsg_graph_create_csr", "qsg_graph_destroy", "qsg_graph_info",
     "qsg_graph_export", "qsg_decode_syndromes", "qsg_decode_syndromes_packed", "qsg_decode_frames",
     "qsg_sample_errors",
-    "qsg_syndromes_of", "qsg_last_error", "qsg_abi_version",
+    "qsg_syndromes_of", "qsg_graph_check_commute", "qsg_last_error", "qsg_abi_version",
 )
 
 
@@ -85,6 +85,7 @@ def lib():
         L.qsg_decode_frames.argtypes = [vp, vp, dbl, dbl, u64, i64, i64, vp, vp, vp, vp, vp]
         L.qsg_sample_errors.argtypes = [i32, dbl, u64, i64, i64, vp, i32, vp]
         L.qsg_syndromes_of.argtypes = [vp, vp, i64, vp, vp]
+        L.qsg_graph_check_commute.argtypes = [vp, vp, vp]
         L.qsg_last_error.restype = C.c_char_p
         L.qsg_last_error.argtypes = []
         L.qsg_abi_version.argtypes = []

@@ -240,7 +240,9 @@ def random_gb_spec(ell: int, w: int, seed: int, max_draws: int = 10_000) -> GbSp
     without replacement from [1, ell) by ``numpy.random.default_rng(seed)``;
     a draw with k = 0 is rejected and redrawn from the same generator.  The
     reference has no such generator; this rule is the
-    builder's definition and is pinned by tests/test_codes.py.
+    builder's definition, and the exact exponent tuples it returns for every
+    BASELINE config-3/4/5 code are pinned by
+    tests/test_host_logic.py::test_random_gb_spec_pinned_codes.
     """
     if w < 1 or w > ell:
         raise ValueError("need 1 <= w <= ell")
@@ -268,9 +270,17 @@ class CodeFormatError(ValueError):
         super().__init__((f"line {line}: " if line is not None else "") + message)
 
 
-def load_qpc(path) -> CodeGraph:
-    """Parse a QPC 1 file into a CodeGraph (validation errors carry line
-    numbers like code.py:292-378; commutation is checked by ``check_commute``)."""
+class OrthogonalityError(ValueError):
+    """Rows of a claimed stabilizer matrix do not all commute (code.py:44-45)."""
+
+
+def load_qpc(path, validate: bool = True) -> CodeGraph:
+    """Parse a QPC 1 file into a CodeGraph (``load_code``, code.py:292-378).
+
+    Malformed content raises CodeFormatError with the line number; with
+    ``validate`` (the reference default) rows that do not all commute raise
+    OrthogonalityError, as ``SparseCheckMatrix.validate(stabilizer=True)``
+    does (code.py:80-97, :375-377)."""
     lines = []
     for num, raw in enumerate(Path(path).read_text(encoding="utf-8").splitlines(), start=1):
         text = raw.split("#", 1)[0].strip()
@@ -332,6 +342,8 @@ def load_qpc(path) -> CodeGraph:
         rows.append(row)
     g = csr_graph(n, rows)
     g.gb = gb
+    if validate and not check_commute(g):
+        raise OrthogonalityError("rows do not commute (H Λ H^T != 0 over GF(2))")
     return g
 
 
@@ -347,7 +359,9 @@ def save_qpc(graph: CodeGraph, path) -> None:
 
 
 def check_commute(graph: CodeGraph) -> bool:
-    """True iff all rows commute (symplectic inner products vanish)."""
+    """True iff all rows commute (symplectic inner products vanish) --
+    pauli.check_orthogonality (pauli.py:120-144) by column intersection on
+    the host, O(m d_c d_v); ``check_commute_device`` is the GPU version."""
     cols = [dict(r) for r in graph.rows]
     by_col: dict[int, list[int]] = {}
     for i, r in enumerate(cols):
@@ -364,3 +378,15 @@ def check_commute(graph: CodeGraph) -> bool:
             return False
     return True
 
+
+
+def check_commute_device(graph, device=None) -> tuple[bool, tuple[int, int] | None]:
+    """Row commutation on the GPU (``qsg_graph_check_commute``): one thread
+    per check, each pair of rows sharing a column evaluated once.  Returns
+    (commutes, lowest anticommuting pair or None)."""
+    from .device import device_graph
+    dg = device_graph(graph, device)
+    ok = C.c_int32()
+    pair = np.zeros(2, dtype=np.int64)
+    _native.check(_native.lib().qsg_graph_check_commute(dg.handle, C.byref(ok), pair.ctypes.data))
+    return bool(ok.value), (None if ok.value else (int(pair[0]), int(pair[1])))

@@ -201,7 +201,15 @@ int compile_layout(qsg_graph *g, int32_t n, int32_t m, const int64_t *cn_ptr, co
         g->nw = (g->ell + 31) / 32;
         const int lpw = g->threads / (2 * g->nw);  // lanes per syndrome word
         if (lpw < 1) {
+            // too few threads for one lane per syndrome word (only reachable
+            // through QSG_THREADS): the generic kernels, with their own
+            // thread rule and no circulant description
             kind = 0;
+            g->ell = g->nw = g->lpw = 0;
+            for (int k = 0; k < 8; ++k) g->gb_a[k] = g->gb_b[k] = 0;
+            if (nodes <= 32 * 12) g->threads = 32;
+            else if (m <= 128 * 32) g->threads = 128;
+            else return fail(QSG_EUNSUPPORTED, "more than 4096 checks");
         } else {
             int p2 = 1;
             while (p2 * 2 <= lpw && p2 * 2 <= 32) p2 *= 2;
@@ -333,14 +341,34 @@ void thresholds(double eps, uint64_t K[3])
     K[2] = (uint64_t)std::ceil(t_z * 9007199254740992.0);
 }
 
+// The dynamic shared-memory limit is an attribute of the kernel FUNCTION
+// (per device), and many graphs share one function; it is raised once to the
+// device's opt-in maximum and never lowered, so no graph's launch can find it
+// set below its own footprint by another graph (or another thread).  The
+// launch's own smem argument still decides occupancy.
+std::mutex g_attr_mu;
+std::vector<std::pair<void *, int>> g_attr_done;
+
+int raise_smem_limit(void *fn, int device, int max_smem)
+{
+    std::lock_guard<std::mutex> lock(g_attr_mu);
+    for (const auto &d : g_attr_done)
+        if (d.first == fn && d.second == device) return QSG_OK;
+    QSG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+    g_attr_done.emplace_back(fn, device);
+    return QSG_OK;
+}
+
 // Pick groups-per-CTA maximising resident frames per SM for one kernel.
 int launch_cfg(qsg_graph *g, bool bp4, bool add, void *fn, qsg::LaunchCfg *out)
 {
+    int max_smem = 0;
+    QSG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
+    int rc = raise_smem_limit(fn, g->device, max_smem);
+    if (rc) return rc;
     std::lock_guard<std::mutex> lock(g->mu);
     qsg::LaunchCfg &c = g->cfg_cache[bp4][add];
     if (c.ok) { *out = c; return QSG_OK; }
-    int max_smem = 0;
-    QSG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
     const int T = g->threads;
     int gmax = 640 / T;           // __launch_bounds__(640)
     int cap_sm = 1 << 30;         // QSG_MAX_FRAMES_PER_SM: tuning/diagnostics only
@@ -349,7 +377,6 @@ int launch_cfg(qsg_graph *g, bool bp4, bool add, void *fn, qsg::LaunchCfg *out)
     for (int G = 1; G <= gmax; ++G) {
         const size_t smem = g->tab_bytes + (size_t)G * g->group_bytes;
         if (smem > (size_t)max_smem) break;
-        QSG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         int nb = 0;
         QSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, G * T, smem));
         nb = std::min(nb, cap_sm / G);
@@ -358,7 +385,6 @@ int launch_cfg(qsg_graph *g, bool bp4, bool add, void *fn, qsg::LaunchCfg *out)
         }
     }
     if (!best.ok) return fail(QSG_EUNSUPPORTED, "graph does not fit in shared memory");
-    QSG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)best.smem));
     c = best;
     *out = best;
     return QSG_OK;
@@ -378,15 +404,16 @@ int launch_decode(qsg_graph *g, const qsg_decoder_cfg *cfg, qsg::KParams &p, cud
     const int64_t want = (p.count + lc.groups - 1) / lc.groups;
     const int grid = (int)std::min<int64_t>(want, (int64_t)lc.ctas_per_sm * g->num_sms);
     unsigned long long *queue = nullptr;
-    {
-        std::lock_guard<std::mutex> lock(g->mu);
-        auto it = g->queues.find(st);
-        if (it == g->queues.end()) {
-            QSG_CUDA(cudaMalloc((void **)&queue, sizeof(unsigned long long)));
-            g->queues.emplace(st, queue);
-        } else {
-            queue = it->second;
-        }
+    // the zeroing of the stream's frame-queue counter and the launch that
+    // consumes it are enqueued under the graph lock, so two host threads
+    // sharing (graph, stream) cannot interleave memset, memset, kernel, kernel
+    std::lock_guard<std::mutex> lock(g->mu);
+    auto it = g->queues.find(st);
+    if (it == g->queues.end()) {
+        QSG_CUDA(cudaMalloc((void **)&queue, sizeof(unsigned long long)));
+        g->queues.emplace(st, queue);
+    } else {
+        queue = it->second;
     }
     QSG_CUDA(cudaMemsetAsync(queue, 0, sizeof(unsigned long long), st));
     p.queue = queue;
@@ -481,6 +508,47 @@ __global__ void syndrome_kernel(int32_t n, int32_t m, const int32_t *cn_ptr, con
             x ^= ((c & 1u) & (s >> 1)) ^ ((c >> 1) & (s & 1u));
         }
         syn[t] = (uint8_t)x;
+    }
+}
+
+// Row commutation (pauli.py:120-144 check_orthogonality, decoder-independent
+// code validation): one thread per check i visits every check k > i sharing
+// a column with it through the qubit lists, and evaluates the pair ONCE --
+// at their first shared column -- by merging the two sorted rows and XORing
+// trace_inner over the shared columns (pauli.py symplectic form: X=1, Z=2,
+// Y=3; two Paulis anticommute iff x1 z2 ^ z1 x2).  O(m d_c d_v (2 d_c))
+// instead of the reference's O(m^2) pair scan.  The lowest anticommuting pair
+// (i * m + k) is kept with atomicMin, so the report is deterministic.
+__global__ void commute_kernel(int32_t m, const int32_t *cn_ptr, const int32_t *edge_vn, const uint8_t *edge_sym,
+                               const int32_t *vn_ptr, const int32_t *vn_order, const int32_t *edge_cn,
+                               unsigned long long *first_bad)
+{
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+        const int b0 = cn_ptr[i], b1 = cn_ptr[i + 1];
+        for (int e = b0; e < b1; ++e) {
+            const int j = edge_vn[e];
+            for (int q = vn_ptr[j]; q < vn_ptr[j + 1]; ++q) {
+                const int e2 = vn_order[q];
+                const int k = edge_cn[e2];
+                if (k <= i) continue;
+                // merge rows i and k: parity over shared columns, first shared column
+                int a = b0, b = cn_ptr[k];
+                const int a1 = b1, bend = cn_ptr[k + 1];
+                int first = -1;
+                uint32_t par = 0;
+                while (a < a1 && b < bend) {
+                    const int ca = edge_vn[a], cb = edge_vn[b];
+                    if (ca < cb) { ++a; continue; }
+                    if (cb < ca) { ++b; continue; }
+                    if (first < 0) first = ca;
+                    const uint32_t s = edge_sym[a], t = edge_sym[b];
+                    par ^= ((s & 1u) & (t >> 1)) ^ ((s >> 1) & (t & 1u));
+                    ++a; ++b;
+                }
+                if (first == j && par)
+                    atomicMin(first_bad, (unsigned long long)i * (unsigned long long)m + (unsigned long long)k);
+            }
+        }
     }
 }
 
@@ -604,6 +672,41 @@ int qsg_graph_export(const qsg_graph *g, int64_t *edge_cn, int64_t *edge_vn, uin
     };
     cp(edge_cn, g->edge_cn); cp(edge_vn, g->edge_vn); cp(edge_sym, g->edge_sym);
     cp(cn_ptr, g->cn_ptr); cp(vn_order, g->vn_order); cp(vn_ptr, g->vn_ptr);
+    return QSG_OK;
+}
+
+int qsg_graph_check_commute(const qsg_graph *g, int32_t *commutes, int64_t *bad_pair)
+{
+    if (!g) return fail(QSG_EINVAL, "null graph");
+    if (g->device < 0) return fail(QSG_EINVAL, "graph was created host-only (device -1)");
+    if (!commutes) return fail(QSG_EINVAL, "null output");
+    DeviceGuard dg(g->device);
+    std::vector<int32_t> vp(g->vn_ptr.begin(), g->vn_ptr.end()), vo(g->vn_order.begin(), g->vn_order.end()),
+        ec(g->edge_cn.begin(), g->edge_cn.end());
+    int32_t *d_vp = nullptr, *d_vo = nullptr, *d_ec = nullptr;
+    unsigned long long *d_bad = nullptr;
+    const unsigned long long none = ~0ull;
+    unsigned long long bad = none;
+    int rc = QSG_OK;
+    cudaError_t err = cudaSuccess;
+    if ((rc = upload(&d_vp, vp)) || (rc = upload(&d_vo, vo)) || (rc = upload(&d_ec, ec))) goto done;
+    if ((err = cudaMalloc((void **)&d_bad, sizeof(bad))) != cudaSuccess ||
+        (err = cudaMemcpy(d_bad, &none, sizeof(none), cudaMemcpyHostToDevice)) != cudaSuccess)
+        goto done;
+    commute_kernel<<<(g->m + 127) / 128, 128>>>(g->m, g->d_cn_ptr, g->d_edge_vn, g->d_edge_sym, d_vp, d_vo, d_ec,
+                                                  d_bad);
+    if ((err = cudaGetLastError()) != cudaSuccess ||
+        (err = cudaMemcpy(&bad, d_bad, sizeof(bad), cudaMemcpyDeviceToHost)) != cudaSuccess)
+        goto done;
+    *commutes = bad == none ? 1 : 0;
+    if (bad_pair) {
+        bad_pair[0] = bad == none ? -1 : (int64_t)(bad / (unsigned long long)g->m);
+        bad_pair[1] = bad == none ? -1 : (int64_t)(bad % (unsigned long long)g->m);
+    }
+done:
+    cudaFree(d_vp); cudaFree(d_vo); cudaFree(d_ec); cudaFree(d_bad);
+    if (rc) return rc;
+    if (err != cudaSuccess) return fail(QSG_ECUDA, std::string("check_commute: ") + cudaGetErrorString(err));
     return QSG_OK;
 }
 

@@ -82,7 +82,19 @@ def test_gpu_outcomes_vs_reference_batches(P, oracle, cname, vn_mode, variant):
         assert np.array_equal(a, c)
     r64 = oracle.decode(g, syn, P.prior_llr(float(eps)).llr, cfg, precision=64, trace=True)
     diff64 = (r32.success != r64.success) | (r32.iterations != r64.iterations) | (r32.e_hat != r64.e_hat).any(axis=1)
-    if variant != "bp4":
+    if variant == "bp4":
+        # numpy's BP4 uses SIMD expm1/log1p, so the fp64 restatement matches
+        # the reference's outcomes on all but <= 2% of frames (iterations
+        # only, tests/test_oracle_pins.py).  The frames where the GPU differs
+        # from the reference are exactly the fp32-vs-fp64 frames (each one
+        # attributed on CPU) except those where the fp64 restatement itself
+        # differs from the reference's libm -- a complete partition:
+        ref64 = (r64.success != b[key + "/success"]) | (r64.iterations != b[key + "/iterations"]) \
+            | (r64.e_hat != b[key + "/e_hat"]).any(axis=1)
+        assert not (~same & ~diff64).any()
+        assert not (same & diff64 & ~ref64).any()
+        assert ref64.mean() <= 0.02 and not (r64.success != b[key + "/success"]).any()
+    else:
         assert np.array_equal(~same, diff64)
         # where fp32 and fp64 trajectories coincide, the GPU's gamma traces
         # are the reference's

@@ -1,0 +1,245 @@
+"""GPU runs of the reference's own correctness suites, restated against the
+device path, and launch-path robustness:
+
+  * cycle-free exactness (reference test_decoder.py:413-469): marginal BP4 on
+    random trees converges to the exact subtree LLRs of the exhaustive
+    posterior (oracle/exhaustive.py restates tests/oracles.py:116-173), and
+    the final hard decisions are the per-qubit MAP decisions;
+  * acceptance criterion 9, safety under fuzzing (test_acceptance.py:272-324):
+    10^4 decodes of random GB / tree codes with random decoders, priors and
+    syndromes -- gamma finite and in [0, 1], success => zero residual, finite
+    messages -- and, beyond the reference, every batch bit-exact against the
+    fp32 oracle;
+  * the on-device commutation check (qsg_graph_check_commute) against the
+    host check and a brute-force pair scan;
+  * kernels shared by graphs of different shared-memory footprints, the
+    too-few-threads fallback to the generic kernels, and concurrent host
+    threads decoding on one (graph, stream).
+"""
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GB254, GB1022, make_tree_rows
+
+pytestmark = pytest.mark.gpu
+
+# fp32 tolerance of the tree-exactness checks: |got - exact| <= TOL max(1, |exact|).
+# The reference asserts 1e-9 for its float64 decoder; the fp32 restatement
+# (== this GPU path bit for bit) measures <= 4e-7 on these trees
+# (tests/test_oracle_pins.py::test_tree_exactness_fp32_oracle).
+TREE_TOL = 2e-6
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2605_10433_b200 as P
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    return P
+
+
+def _hd_metrics(g, cn, l0):
+    """(n, 4) decision metrics of decoder.py:292-301 in float64 from the
+    final check->qubit messages (canonical edge order)."""
+    cv = np.asarray(cn, dtype=np.float64)[g.vn_order]
+    sym = g.edge_sym[g.vn_order].astype(np.int64)
+    sx, sz = sym & 1, sym >> 1
+    m = np.zeros((g.n, 4))
+    for e, anti in ((1, sz), (2, sx), (3, sx ^ sz)):
+        m[:, e] = l0 + np.add.reduceat(cv * anti, g.vn_ptr[:-1])
+    return m
+
+
+def test_marginal_bp4_exact_on_trees(P):
+    """test_decoder.py:413-440 on the GPU (fp32 tolerance)."""
+    from oracle import exhaustive as X
+    rng = np.random.default_rng(2024)
+    for trial in range(6):
+        n, rows = make_tree_rows(rng, int(rng.integers(5, 9)))
+        g = P.csr_graph(n, rows)
+        eps0 = float(rng.uniform(0.03, 0.25))
+        prior = P.prior_llr(eps0)
+        truth = np.array([rng.choice(4, p=[1 - eps0] + [eps0 / 3] * 3) for _ in range(n)], dtype=np.uint8)
+        s = g.syndromes_of(truth)[0]
+        cfg = P.DecoderConfig("bp4", l_max=2 * n, vn_mode="marginal")
+        r = P.decode(None, g, s, prior, cfg, capture_messages=True, early_stop=False)
+        final = r.message_trace[-1]
+        exact = X.brute_vn_messages(n, rows, s, eps0, g.edges)
+        got = np.asarray(final.vn_to_cn, dtype=np.float64)
+        err = np.abs(got - exact) / np.maximum(1.0, np.abs(exact))
+        assert err.max() <= TREE_TOL, (trial, float(err.max()))
+        hd = np.argmin(_hd_metrics(g, final.cn_to_vn, prior.llr), axis=1)
+        assert np.array_equal(hd, X.map_decisions(n, rows, s, eps0)), trial
+
+
+def test_marginal_bp4_beliefs_match_posteriors_on_tree(P):
+    """test_decoder.py:443-469 on the GPU: decision metrics are shifted
+    negative log posteriors."""
+    from oracle import exhaustive as X
+    rng = np.random.default_rng(7)
+    n, rows = make_tree_rows(rng, 7)
+    g = P.csr_graph(n, rows)
+    eps0 = 0.1
+    prior = P.prior_llr(eps0)
+    truth = np.array([0, 1, 0, 0, 2, 0, 3][:n], dtype=np.uint8)
+    s = g.syndromes_of(truth)[0]
+    cfg = P.DecoderConfig("bp4", l_max=2 * n, vn_mode="marginal")
+    r = P.decode(None, g, s, prior, cfg, capture_messages=True, early_stop=False)
+    m = _hd_metrics(g, r.message_trace[-1].cn_to_vn, prior.llr)
+    marg = X.posterior_marginals(n, rows, s, eps0)
+    checked = 0
+    for j in range(n):
+        for e in range(1, 4):
+            if marg[j, e] > 1e-12 and marg[j, 0] > 1e-12:
+                want = np.log(marg[j, 0] / marg[j, e])
+                assert abs(m[j, e] - want) <= TREE_TOL * max(1.0, abs(want)), (j, e)
+                checked += 1
+    assert checked > 0
+
+
+def test_criterion_9_safety_under_fuzzing(P, oracle):
+    """test_acceptance.py:272-324 (same generator stream, seed 4242) on the
+    device path, plus bit-exactness of every batch against the fp32 oracle."""
+    rng = np.random.default_rng(4242)
+    total = batches = 0
+    while total < 10_000:
+        if rng.random() < 0.7:
+            ell = int(rng.integers(2, 9))
+            a = tuple(sorted(rng.choice(ell, size=int(rng.integers(1, min(4, ell) + 1)), replace=False).tolist()))
+            b = tuple(sorted(rng.choice(ell, size=int(rng.integers(1, min(4, ell) + 1)), replace=False).tolist()))
+            g = P.gb_graph(P.GbSpec(ell, a, b))
+        else:
+            n, rows = make_tree_rows(rng, int(rng.integers(4, 12)))
+            g = P.csr_graph(n, rows)
+        variant = ("bp4", "ms", "sms", "sagms")[int(rng.integers(0, 4))]
+        kw = {}
+        if variant == "sms":
+            kw["alpha"] = float(rng.uniform(0.05, 1.0))
+        if variant == "sagms":
+            amax = float(rng.uniform(0.2, 0.9))
+            amin = float(rng.uniform(0.05, amax))
+            eta = float(rng.uniform(1.0, 1.0 / amax))
+            kw["gain"] = P.GainParams(amin, amax, eta)
+        cfg = P.DecoderConfig(variant, l_max=int(rng.integers(1, 12)),
+                              vn_mode=("marginal", "additive")[int(rng.integers(0, 2))], **kw)
+        prior = P.prior_llr(float(rng.uniform(0.005, 0.6)))
+        count = 170
+        syn = rng.integers(0, 2, size=(count, g.m)).astype(np.uint8)
+        res = P.decode_batch(g, syn, prior, cfg, collect_gamma=True)
+        total += count
+        batches += 1
+        for t in res.gamma_traces:
+            assert np.isfinite(t).all() and (t >= 0).all() and (t <= 1).all()
+        resid = g.syndromes_of(res.e_hat) ^ syn
+        assert not resid[res.success].any()
+        probe = P.decode(None, g, syn[0], prior, cfg, capture_messages=True)
+        for st in probe.message_trace or []:
+            assert np.isfinite(st.vn_to_cn).all() and np.isfinite(st.cn_to_vn).all()
+        want = oracle.decode(g, syn, prior.llr, cfg, precision=32)
+        assert np.array_equal(res.success, want.success) and np.array_equal(res.iterations, want.iterations)
+        assert np.array_equal(res.e_hat, want.e_hat)
+    assert total >= 10_000 and batches >= 59
+
+
+def _commute_pairs_brute(g):
+    """Lowest anticommuting (i, k) by the reference's O(m^2) pair scan
+    (pauli.py:120-144), or None."""
+    rows = [dict(r) for r in g.rows]
+    for i in range(g.m):
+        for k in range(i + 1, g.m):
+            acc = 0
+            for j, s in rows[i].items():
+                t = rows[k].get(j)
+                if t is not None:
+                    acc ^= ((s & 1) & (t >> 1)) ^ ((s >> 1) & (t & 1))
+            if acc:
+                return (i, k)
+    return None
+
+
+def test_check_commute_device(P):
+    from test_host_logic import PINNED_RANDOM_GB
+    for spec in [GB254, GB1022] + [(l, a, b) for (l, _), (a, b) in PINNED_RANDOM_GB.items()]:
+        ok, pair = P.check_commute_device(P.gb_graph(P.GbSpec(*spec)))
+        assert ok and pair is None, spec
+    rng = np.random.default_rng(5)
+    seen = set()
+    for t in range(60):
+        n, m = int(rng.integers(4, 12)), int(rng.integers(2, 9))
+        while True:
+            picks = [sorted(rng.choice(n, size=int(rng.integers(2, min(n, 5) + 1)), replace=False).tolist())
+                     for _ in range(m)]
+            if len(set(sum(picks, []))) == n:
+                break
+        rows = [[(j, int(rng.integers(1, 4))) for j in cols] for cols in picks]
+        g = P.csr_graph(n, rows)
+        ok, pair = P.check_commute_device(g)
+        want = _commute_pairs_brute(g)
+        assert ok == (want is None) == P.check_commute(g), t
+        assert pair == want, t
+        seen.add(ok)
+    assert seen == {True, False}
+    # a GB code with one symbol flipped no longer commutes
+    g = P.gb_graph(P.GbSpec(*GB254))
+    sym = g.edge_sym.copy()
+    sym[3] = 3
+    bad = P.CodeGraph(n=g.n, m=g.m, edge_cn=g.edge_cn, edge_vn=g.edge_vn, edge_sym=sym, cn_ptr=g.cn_ptr,
+                      vn_order=g.vn_order, vn_ptr=g.vn_ptr)
+    ok, pair = P.check_commute_device(bad)
+    assert not ok and pair == _commute_pairs_brute(bad)
+
+
+def test_graphs_sharing_a_kernel_with_different_footprints(P, oracle):
+    """W = 5 codes at l = 127 and l = 96 run the same decode_kernel<5,32,..,256>
+    instance with different dynamic shared memory; launching A, B, A (and B
+    again) must never trip the per-function shared-memory limit."""
+    a = P.gb_graph(P.GbSpec(*GB254))
+    b = P.gb_graph(P.GbSpec(96, (0, 5, 17, 40, 71), (0, 9, 33, 60, 88)))
+    assert P.device_graph(a).kind == P.device_graph(b).kind == 5
+    cfg = P.DecoderConfig("sagms", l_max=30, gain=P.GainParams(0.30, 0.50, 1.10))
+    for g in (a, b, a, b):
+        f, it = P.decode_frames(g, cfg, 0.06, 0.06, 1, 0, 500)
+        of, oi, _, _ = oracle.frames(g, cfg, 0.06, 0.06, 1, 0, 500)
+        assert np.array_equal(f, of) and np.array_equal(it, oi)
+
+
+def test_too_few_threads_falls_back_to_generic(P, oracle, monkeypatch):
+    """QSG_THREADS=32 at l = 600 leaves < 1 lane per syndrome word: the
+    layout compiler must switch to the generic kernels with their own thread
+    rule (not keep 32 threads for 1200 checks)."""
+    monkeypatch.setenv("QSG_THREADS", "32")
+    g = P.gb_graph(P.random_gb_spec(600, 4, seed=1))
+    dg = P.device_graph(g)
+    assert dg.kind == 0 and dg.threads == 128
+    cfg = P.DecoderConfig("sms", l_max=15, alpha=0.75)
+    f, it = P.decode_frames(g, cfg, 0.05, 0.05, 3, 0, 64)
+    of, oi, _, _ = oracle.frames(g, cfg, 0.05, 0.05, 3, 0, 64)
+    assert np.array_equal(f, of) and np.array_equal(it, oi)
+
+
+def test_concurrent_host_threads_on_one_stream(P):
+    """ctypes releases the GIL: host threads decoding the same graph on the
+    same (default) stream must each get their own complete frame range."""
+    g = P.gb_graph(P.GbSpec(*GB254))
+    cfg = P.DecoderConfig("sagms", l_max=100, gain=P.GainParams(0.30, 0.50, 1.10))
+    want = {k: P.decode_frames(g, cfg, 0.06, 0.06, 0, 5000 * k, 5000) for k in range(6)}
+    got, errors = {}, []
+
+    def work(k):
+        try:
+            for _ in range(3):
+                got[k] = P.decode_frames(g, cfg, 0.06, 0.06, 0, 5000 * k, 5000)
+                assert np.array_equal(got[k][0], want[k][0]) and np.array_equal(got[k][1], want[k][1])
+        except Exception as exc:  # surfaced below
+            errors.append((k, repr(exc)))
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(6)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors

@@ -147,6 +147,72 @@ def test_random_gb_spec():
         assert P.gb_graph(s).kind in (0, w)
 
 
+# random_gb_spec(ell, w, seed=0) for every BASELINE config-3/4/5 code: the
+# generator is the builder's definition (the reference ships none), so its
+# exact output is pinned here -- any change to the draw rule shows up.
+PINNED_RANDOM_GB = {
+    (63, 5): ((0, 17, 32, 39, 51), (0, 1, 11, 41, 50)),
+    (127, 5): ((0, 10, 34, 56, 88), (0, 3, 90, 108, 117)),
+    (255, 5): ((0, 20, 72, 105, 187), (0, 30, 34, 47, 234)),
+    (511, 5): ((0, 5, 200, 397, 418), (0, 81, 284, 347, 418)),
+    (127, 3): ((0, 9, 74), (0, 13, 80)),
+    (127, 4): ((0, 65, 80, 106), (0, 3, 6, 10)),
+    (127, 6): ((0, 34, 39, 64, 79, 104), (0, 63, 77, 80, 100, 114)),
+    (127, 8): ((0, 6, 10, 34, 39, 63, 78, 103), (0, 68, 70, 73, 78, 89, 118, 126)),
+}
+
+
+def test_random_gb_spec_pinned_codes():
+    for (ell, w), (a, b) in PINNED_RANDOM_GB.items():
+        s = P.random_gb_spec(ell, w, seed=0)
+        assert (s.ell, s.a_exponents, s.b_exponents) == (ell, a, b), (ell, w)
+        k = P.gb_dimension(s)
+        assert k > 0 and k == P.code_dimension(P.gb_graph(s))
+        assert P.check_commute(P.gb_graph(s))
+
+
+def test_load_qpc_validates_commutation(tmp_path):
+    """load_code(validate=True) raises OrthogonalityError for rows that do
+    not commute (code.py:375-377, :96-97); validate=False loads them."""
+    (tmp_path / "anti.qpc").write_text("QPC 1\nn=2 m=2\n0: 0:X 1:X\n1: 0:Z\n")
+    with pytest.raises(P.OrthogonalityError):
+        P.load_qpc(tmp_path / "anti.qpc")
+    g = P.load_qpc(tmp_path / "anti.qpc", validate=False)
+    assert g.m == 2 and not P.check_commute(g)
+    # X X / Z Z commute (two anticommuting positions)
+    (tmp_path / "ok.qpc").write_text("QPC 1\nn=2 m=2\n0: 0:X 1:X\n1: 0:Z 1:Z\n")
+    assert P.check_commute(P.load_qpc(tmp_path / "ok.qpc"))
+    assert issubclass(P.OrthogonalityError, ValueError) and P.load_code is P.load_qpc
+
+
+def test_load_qpc_validation_matches_reference(reference, tmp_path):
+    from qsagms.code import OrthogonalityError, load_code
+    rng = np.random.default_rng(11)
+    seen = set()
+    for t in range(40):
+        n, m = 6, 4
+        while True:  # every qubit covered (the layout compiler rejects isolated qubits)
+            picks = [sorted(rng.choice(n, size=rng.integers(2, 5), replace=False).tolist()) for _ in range(m)]
+            if len(set(sum(picks, []))) == n:
+                break
+        rows = [" ".join(f"{j}:{'XZY'[rng.integers(0, 3)]}" for j in cols) for cols in picks]
+        text = "QPC 1\nn=6 m=4\n" + "".join(f"{i}: {r}\n" for i, r in enumerate(rows))
+        (tmp_path / f"r{t}.qpc").write_text(text)
+        try:
+            load_code(tmp_path / f"r{t}.qpc")
+            ref_ok = True
+        except OrthogonalityError:
+            ref_ok = False
+        try:
+            P.load_qpc(tmp_path / f"r{t}.qpc")
+            ours = True
+        except P.OrthogonalityError:
+            ours = False
+        assert ours == ref_ok, text
+        seen.add(ours)
+    assert seen == {True, False}
+
+
 def test_qpc_roundtrip(tmp_path):
     g = P.gb_graph(P.GbSpec(*GB126))
     P.save_qpc(g, tmp_path / "c.qpc")

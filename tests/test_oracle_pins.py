@@ -150,7 +150,12 @@ def test_restatements_vs_reference_batches(oracle, batches, cname, vn_mode, vari
         gam = np.concatenate(r64.gamma_traces(g.m))
         assert np.array_equal(gam, batches[key + "/gamma"])
     else:
-        assert (r64.success != ref_succ).mean() <= 0.05
+        # numpy's BP4 runs SIMD expm1/log1p (not glibc): success and e_hat
+        # still equal on every frame; iteration counts differ on <= 2% of
+        # frames (4 of 200 on small/marginal, 0 elsewhere)
+        assert np.array_equal(r64.success, ref_succ)
+        assert np.array_equal(r64.e_hat, ref_eh)
+        assert (r64.iterations != ref_it).mean() <= 0.02
     # fp32 vs fp64 outcome differences: every one is attributed to a tie
     # broken by rounding in tests/test_attribution.py
 
@@ -200,3 +205,61 @@ def test_bp4_closed_form(oracle):
     # ext floor phi(1e-12)
     assert np.all(oracle.bp4_mags(np.float32([0.0, 2.0, 3.0]))[1:] == np.float32(3.8574998e-22))
     assert oracle.bp4_mags(np.float32([1.5]))[0] == np.float32(28.32417)
+
+def _ref_oracles():
+    """The reference's own test oracles (tests/oracles.py), imported from the
+    read-only tree (CPU container only)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("ref_oracles", "/root/reference/pkg/tests/oracles.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def test_exhaustive_oracle_matches_reference(reference):
+    """oracle/exhaustive.py (the tree-exactness ground truth the GPU suite
+    uses) equals the reference's tests/oracles.py:116-173 bit for bit."""
+    from qsagms.code import SparseCheckMatrix
+
+    from conftest import make_tree_rows
+    from oracle import exhaustive as X
+    R = _ref_oracles()
+    rng = np.random.default_rng(99)
+    for t in range(5):
+        n, rows = make_tree_rows(rng, int(rng.integers(4, 8)))
+        H = SparseCheckMatrix(n=n, rows=rows)
+        eps0 = float(rng.uniform(0.03, 0.25))
+        e = rng.integers(0, 4, size=n).astype(np.uint8)
+        s = R.syndrome_dense(H, e)
+        assert np.array_equal(X.posterior_marginals(n, rows, s, eps0), R.posterior_marginals(H, s, eps0))
+        assert np.array_equal(X.map_decisions(n, rows, s, eps0), R.map_decisions(H, s, eps0))
+        for i, row in enumerate(rows):
+            for j, _ in row:
+                assert X.brute_vn_message(n, rows, s, eps0, i, j) == R.brute_vn_message(H, s, eps0, i, j)
+
+
+@pytest.mark.parametrize("precision,tol", [(64, 1e-9), (32, 2e-6)])
+def test_tree_exactness_oracle(oracle, precision, tol):
+    """Reference test_decoder.py:413-440 on both restatements: converged BP4
+    messages equal the exhaustive subtree LLRs (fp64 within the reference's
+    1e-9; fp32 -- the GPU's arithmetic bit for bit -- within 2e-6 relative,
+    unit floor; measured <= 4e-7) and the final decisions are MAP."""
+    from conftest import make_tree_rows
+    from oracle import exhaustive as X
+    rng = np.random.default_rng(2024)
+    for trial in range(6):
+        n, rows = make_tree_rows(rng, int(rng.integers(5, 9)))
+        g = oracle.tanner_arrays(n, rows)
+        eps0 = float(rng.uniform(0.03, 0.25))
+        l0 = oracle.prior_llr(eps0)
+        truth = np.array([rng.choice(4, p=[1 - eps0] + [eps0 / 3] * 3) for _ in range(n)], dtype=np.uint8)
+        s = oracle.syndromes_of(g, truth[None])[0]
+        c = NS(variant="bp4", l_max=2 * n, vn_mode="marginal", alpha=None, gain=None)
+        r = oracle.decode(g, s[None], l0, c, precision=precision, capture=True, early_stop=False)
+        k = int(r.counts[0, 1]) - 1
+        exact = X.brute_vn_messages(n, rows, s, eps0, g.edges)
+        got = r.vn_msgs[0, k].astype(np.float64)
+        assert (np.abs(got - exact) / np.maximum(1.0, np.abs(exact))).max() <= tol, trial
+        from oracle.attribution import _metrics
+        hd = np.argmin(_metrics(oracle.Graph(g), r.cn_msgs[0, k], l0, np.float64), axis=1)
+        assert np.array_equal(hd, X.map_decisions(n, rows, s, eps0)), trial
