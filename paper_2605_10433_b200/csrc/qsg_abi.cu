@@ -310,6 +310,7 @@ int compile_layout(qsg_graph *g, int32_t n, int32_t m, const int64_t *cn_ptr, co
     g->off_synw = (uint32_t)off; off += (size_t)8 * g->nw;
     g->off_resw = (uint32_t)off; off += (size_t)8 * g->nw;
     off = (off + 7) / 8 * 8;
+    // scratch: group_sum slots, the frame index (8 B), the per-group tallies (16 B)
     g->off_scratch = (uint32_t)off; off += 2 * (T / 32) * 4 + 8;
     g->group_bytes = (uint32_t)((off + 15) / 16 * 16);
     return QSG_OK;
@@ -370,7 +371,11 @@ int launch_cfg(qsg_graph *g, bool bp4, bool add, void *fn, qsg::LaunchCfg *out)
     qsg::LaunchCfg &c = g->cfg_cache[bp4][add];
     if (c.ok) { *out = c; return QSG_OK; }
     const int T = g->threads;
-    int gmax = 640 / T;           // __launch_bounds__(640)
+    cudaFuncAttributes fa;
+    QSG_CUDA(cudaFuncGetAttributes(&fa, fn));
+    // at most 640 threads per CTA, and no more than the register budget
+    // (__maxnreg__, reg_budget in qsg_kernel.cuh) lets one CTA hold
+    int gmax = std::min(640, fa.maxThreadsPerBlock) / T;
     int cap_sm = 1 << 30;         // QSG_MAX_FRAMES_PER_SM: tuning/diagnostics only
     if (const char *env = std::getenv("QSG_MAX_FRAMES_PER_SM")) cap_sm = std::max(1, std::atoi(env));
     qsg::LaunchCfg best;
@@ -385,6 +390,10 @@ int launch_cfg(qsg_graph *g, bool bp4, bool add, void *fn, qsg::LaunchCfg *out)
         }
     }
     if (!best.ok) return fail(QSG_EUNSUPPORTED, "graph does not fit in shared memory");
+    if (std::getenv("QSG_VERBOSE"))  // diagnostics
+        std::fprintf(stderr, "qsg launch_cfg: kind %d T %d bp4 %d regs %d groups %d ctas/SM %d smem %zu (group %u, tab %u)\n",
+                     g->kind, T, (int)bp4, fa.numRegs, best.groups, best.ctas_per_sm, best.smem, g->group_bytes,
+                     g->tab_bytes);
     c = best;
     *out = best;
     return QSG_OK;

@@ -619,18 +619,24 @@ __device__ __forceinline__ void cn_phase_first(const KParams &p, const GroupMem 
 #pragma unroll 1
     for (int c = tid; c < l; c += T) {
         const int bit = c & 31;
+        // both checks' slot indices first: the stores are volatile (ordered
+        // against the barriers), so a load issued after a store would wait
+        // for it -- one table-load latency per edge otherwise
+        uint32_t ad[2][D];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint16_t *row = reinterpret_cast<const uint16_t *>(gm.tab + (h * l + c) * p.row_words);
+#pragma unroll
+            for (int q = 0; q < D; ++q) ad[h][q] = msg_s + 4u * lds_u16(row + q);
+        }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int wd = h * nw + (c >> 5);
             const uint32_t s = (gm.synw[wd] >> bit) & 1u, r = (gm.resw[wd] >> bit) & 1u;
-            const uint16_t *row = reinterpret_cast<const uint16_t *>(gm.tab + (h * l + c) * p.row_words);
             const uint32_t sg = s << 31;
             const uint32_t ms = (r ? m1 : m0) ^ sg;
 #pragma unroll
-            for (int q = 0; q < D; ++q) {
-                const uint32_t w = BP4 ? (p.first_bp4[q] ^ sg) : ms;
-                sts_a(msg_s + 4u * lds_u16(row + q), w);
-            }
+            for (int q = 0; q < D; ++q) sts_a(ad[h][q], BP4 ? (p.first_bp4[q] ^ sg) : ms);
         }
     }
 }
@@ -654,10 +660,20 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, u
             const uint32_t s1 = gm.synw[wd1] >> bit, r1 = gm.resw[wd1] >> bit;
             uint32_t ad0[D], ad1[D];
             float v0[D], v1[D];
-            cn_load<D>(reinterpret_cast<const uint16_t *>(gm.tab + c * p.row_words), msg_s, ad0, v0);
-            cn_load<D>(reinterpret_cast<const uint16_t *>(gm.tab + (l + c) * p.row_words), msg_s, ad1, v1);
-            cn_finish<D, BP4>(ad0, v0, s0 << 31, (r0 & 1u) ? g1 : g0);
-            cn_finish<D, BP4>(ad1, v1, s1 << 31, (r1 & 1u) ? g1 : g0);
+            if constexpr (BP4) {
+                // one check at a time: the product-form update is long enough
+                // to hide its loads, and the second check's 2D live values
+                // would push the kernel past its register budget
+                cn_load<D>(reinterpret_cast<const uint16_t *>(gm.tab + c * p.row_words), msg_s, ad0, v0);
+                cn_finish<D, BP4>(ad0, v0, s0 << 31, (r0 & 1u) ? g1 : g0);
+                cn_load<D>(reinterpret_cast<const uint16_t *>(gm.tab + (l + c) * p.row_words), msg_s, ad1, v1);
+                cn_finish<D, BP4>(ad1, v1, s1 << 31, (r1 & 1u) ? g1 : g0);
+            } else {
+                cn_load<D>(reinterpret_cast<const uint16_t *>(gm.tab + c * p.row_words), msg_s, ad0, v0);
+                cn_load<D>(reinterpret_cast<const uint16_t *>(gm.tab + (l + c) * p.row_words), msg_s, ad1, v1);
+                cn_finish<D, BP4>(ad0, v0, s0 << 31, (r0 & 1u) ? g1 : g0);
+                cn_finish<D, BP4>(ad1, v1, s1 << 31, (r1 & 1u) ? g1 : g0);
+            }
         }
     } else {
         constexpr uint32_t kAddr = 0x00ffffffu;  // generic entries carry sym << 30
@@ -806,6 +822,109 @@ __device__ __forceinline__ uint32_t vn_update_fixed(unsigned char *col, uint32_t
     return vn_finish<W, ADD, NP>(cs, rowb, c, l0, kapc);
 }
 
+// First qubit update of the min-sum family (marginal VN, bicycle kernels
+// with the closed-form first check update, W <= 5).  After iteration 1's
+// check update every message is +A (satisfied check: g0 min(v0, 64)) or -B
+// (unsatisfied: g1 min(v0, 64)), so a qubit's X-edge sum S_X (numpy tree
+// x0 + ((x1 + x2) + (x3 + x4)) over its W X-edges) and F(S_X) depend only on
+// the W-bit pattern of which of its X checks are unsatisfied -- likewise S_Z
+// and F(S_Z) on the Z-edge pattern.  Lane p of every warp tabulates both for
+// pattern p (2^W <= 32 patterns; the same fp32 recipes, so the table entries
+// are bit-identical to the general update's values), and each qubit fetches
+// its four values with shuffles instead of evaluating the exponential and
+// two logarithms of vn_F2.  The Y-belief sum over all 2W edges, the hard
+// decision and the outgoing messages V - c are computed as in vn_finish.
+// Pattern bit (W - 1 - s) <-> edge s (the funnel-shift packing below).
+template <int W>
+struct FirstTab {
+    float sx, fx, sz, fz;  // this lane's pattern: S_X, F(S_X), S_Z, F(S_Z)
+};
+
+template <int W>
+__device__ __forceinline__ FirstTab<W> first_tab(float A, float nB, float kapc, uint32_t lane)
+{
+    constexpr int D = 2 * W;
+    const uint32_t pat = lane & ((1u << W) - 1u);
+    OptF ox[D], oz[D];
+#pragma unroll
+    for (int s = 0; s < W; ++s) {
+        const float v = (pat >> (W - 1 - s)) & 1u ? nB : A;
+        oz[s] = OptF{v, true};       // X-edge s (anti_Z keeps X-edges)
+        oz[W + s] = OptF{0.0f, false};
+        ox[s] = OptF{0.0f, false};
+        ox[W + s] = OptF{v, true};   // Z-edge s
+    }
+    FirstTab<W> t;
+    t.sz = segsum_c<D>(ox);
+    t.sx = segsum_c<D>(oz);
+    const F2 f = vn_F2(t.sz, t.sx, bc(kapc));
+    t.fz = lo(f);
+    t.fx = hi(f);
+    return t;
+}
+
+// All 32 lanes must call this (shuffles); lanes without a qubit pass
+// store = false (their loads read inside the group's area and are ignored).
+template <int W, int NP>
+__device__ __forceinline__ uint32_t vn_first_fixed(uint32_t cs, uint32_t rowb, float l0, const FirstTab<W> &t,
+                                                   bool store)
+{
+    if constexpr (NP > 0) rowb = 4u * NP;
+    constexpr int D = 2 * W;
+    float c[D];
+    vn_load<W, NP>(cs, rowb, c);
+    uint32_t px = 0, pz = 0;
+#pragma unroll
+    for (int s = 0; s < W; ++s) {
+        px = __funnelshift_l(f2u(c[s]), px, 1);      // (px << 1) | sign(c[s])
+        pz = __funnelshift_l(f2u(c[W + s]), pz, 1);
+    }
+    const float sX = __shfl_sync(0xffffffffu, t.sx, (int)px), fX = __shfl_sync(0xffffffffu, t.fx, (int)px);
+    const float sZ = __shfl_sync(0xffffffffu, t.sz, (int)pz), fZ = __shfl_sync(0xffffffffu, t.fz, (int)pz);
+    OptF oa[D];
+#pragma unroll
+    for (int s = 0; s < D; ++s) oa[s] = OptF{c[s], true};
+    const float bX = l0 + sZ, bZ = l0 + sX;
+    const float bY = l0 + segsum_c<D>(oa);
+    const F2 v2 = add2(pk(bZ, bX), pk(fZ, fX));
+    if (store) {
+#pragma unroll
+        for (int s = 0; s < W; ++s) {
+            const F2 o2 = sub2(v2, pk(c[s], c[W + s]));
+            sts_a(cs + s * rowb, f2u(lo(o2)));
+            sts_a(cs + (W + s) * rowb, f2u(hi(o2)));
+        }
+    }
+    return hard_decision(bX, bZ, bY);
+}
+
+template <int W, int T, int NP>
+__device__ __forceinline__ void vn_phase_first(const KParams &p, const GroupMem &gm, float g0, float g1, int tid)
+{
+    const uint32_t rowb = (uint32_t)p.n_pad * 4;
+    const float a = fminf(p.v0, kClip);
+    // the words cn_phase_first stored: +m0 (satisfied), -m1 (unsatisfied)
+    const float A = fminf(g0 * a, kClip), nB = -fminf(g1 * a, kClip);
+    const FirstTab<W> t = first_tab<W>(A, nB, p.kapc, (uint32_t)tid & 31u);
+    const int l = p.ell, nw1 = p.nw + 1;
+    const float l0 = p.l0;
+#pragma unroll 1
+    for (int c0 = tid & ~31; c0 < l; c0 += T) {
+        const int c = c0 + (tid & 31);
+        const bool ok = c < l;
+        const int cc = ok ? c : c0;  // idle lanes re-read a valid column, store nothing
+        const uint32_t eL = vn_first_fixed<W, NP>(smem_addr(gm.msg + 4 * cc), rowb, l0, t, ok);
+        const uint32_t eR = vn_first_fixed<W, NP>(smem_addr(gm.msg + 4 * (l + cc)), rowb, l0, t, ok);
+        const uint32_t xl = __ballot_sync(0xffffffffu, ok && (eL & 1u)), zl = __ballot_sync(0xffffffffu, ok && (eL >> 1));
+        const uint32_t xr = __ballot_sync(0xffffffffu, ok && (eR & 1u)), zr = __ballot_sync(0xffffffffu, ok && (eR >> 1));
+        if ((tid & 31) == 0) {
+            const int wd = c0 >> 5;
+            gm.bits[kXL * nw1 + wd] = xl; gm.bits[kZL * nw1 + wd] = zl;
+            gm.bits[kXR * nw1 + wd] = xr; gm.bits[kZR * nw1 + wd] = zr;
+        }
+    }
+}
+
 template <int W, int T, bool BP4, bool ADD, int NP>
 __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, int tid)
 {
@@ -946,8 +1065,15 @@ __device__ __forceinline__ uint8_t ehat_of(const KParams &p, const GroupMem &gm,
     }
 }
 
+// Threads-per-CTA bound per W, which sets the register budget: 640 (96
+// registers, 20 warps per SM) for W <= 5; 512 (128) for W = 6 and 384 (168)
+// for W = 8, whose 12 / 16 fp32 messages per qubit slot limit the frames per
+// SM by shared memory anyway (<= 18 / 13) -- under the 640 bound those
+// kernels spilled (BASELINE config 4).
+constexpr int max_threads(int W) { return W == 8 ? 384 : (W == 6 ? 512 : 640); }
+
 template <int W, int T, bool BP4, bool ADD, int NP>
-__global__ void __launch_bounds__(640) decode_kernel(const KParams p)
+__global__ void __launch_bounds__(max_threads(W)) decode_kernel(const KParams p)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     // ---- per-CTA copy of the graph tables ----
@@ -997,18 +1123,23 @@ __global__ void __launch_bounds__(640) decode_kernel(const KParams p)
     }
     const bool capture = p.tr_vn != nullptr || p.tr_cn != nullptr;
 
+    // frame queue: the index of the NEXT frame is fetched as soon as the
+    // current one is known, so the global atomic's round trip overlaps the
+    // current frame's decode instead of stalling the group between frames
+    long long f_next = 0;
+    if (tid == 0) f_next = (long long)atomicAdd(p.queue, 1ull);
     while (true) {
         long long f;
         if constexpr (T == 32) {
-            if (tid == 0) f = (long long)atomicAdd(p.queue, 1ull);
-            f = __shfl_sync(0xffffffffu, f, 0);
+            f = __shfl_sync(0xffffffffu, f_next, 0);
         } else {
-            if (tid == 0) *fslot = (long long)atomicAdd(p.queue, 1ull);
+            if (tid == 0) *fslot = f_next;
             group_sync<T>(g);
             f = *fslot;
             group_sync<T>(g);
         }
         if (f >= p.count) break;
+        if (tid == 0) f_next = (long long)atomicAdd(p.queue, 1ull);
 
         // ---- frame input: observed syndrome ----
         uint32_t syn_bits = 0;
@@ -1025,7 +1156,7 @@ __global__ void __launch_bounds__(640) decode_kernel(const KParams p)
                     for (int q = 0; q < 4; ++q)
                         if (4 * b + q < n) eb[4 * b + q] = pauli_from_word(w.v[q], p.kx, p.ky, p.kz);
                 }
-                for (int w = tid; w < 4 * (p.nw + 1); w += T) gm.bits[w] = 0u;
+                if (tid < 4) gm.bits[tid * (p.nw + 1) + p.nw] = 0u;  // padding words (the rest is written below)
                 group_sync<T>(g);
                 bitmaps_from_bytes<T>(p, gm, eb, tid);
                 group_sync<T>(g);
@@ -1059,12 +1190,12 @@ __global__ void __launch_bounds__(640) decode_kernel(const KParams p)
             }
             // e_hat of iteration 1: hd0 on every qubit
             const int nw1 = p.nw + 1;
-            for (int w = tid; w < 4 * nw1; w += T) {
-                const int wd = w % nw1, blk = w / nw1;
+            for (int wd = tid; wd < nw1; wd += T) {
                 const int valid = p.ell - 32 * wd;
                 const uint32_t full = valid >= 32 ? 0xffffffffu : (valid > 0 ? (1u << valid) - 1u : 0u);
-                const uint32_t bit = (blk == kXL || blk == kXR) ? (hd0 & 1u) : (hd0 >> 1);
-                gm.bits[w] = bit ? full : 0u;
+                const uint32_t x = (hd0 & 1u) ? full : 0u, z = (hd0 >> 1) ? full : 0u;
+                gm.bits[kXL * nw1 + wd] = x; gm.bits[kZL * nw1 + wd] = z;
+                gm.bits[kXR * nw1 + wd] = x; gm.bits[kZR * nw1 + wd] = z;
             }
         } else {
             if (p.sample) {
@@ -1146,7 +1277,14 @@ __global__ void __launch_bounds__(640) decode_kernel(const KParams p)
                 cn_phase<W, T, BP4, NP>(p, gm, syn_bits, res, g0, g1, tid);
             group_sync<T>(g);
             if (capture && p.tr_cn) snapshot<T>(p, gm.msg, p.tr_cn + (f * p.l_max + n_snap) * p.E, tid, false);
-            vn_phase<W, T, BP4, ADD, NP>(p, gm, tid);
+            if constexpr (W > 0 && W <= 5 && !BP4 && !ADD) {
+                if (ell == 1 && p.first_fast)
+                    vn_phase_first<(W > 0 ? W : 1), T, NP>(p, gm, g0, g1, tid);
+                else
+                    vn_phase<W, T, BP4, ADD, NP>(p, gm, tid);
+            } else {
+                vn_phase<W, T, BP4, ADD, NP>(p, gm, tid);
+            }
             group_sync<T>(g);
             if (capture) {
                 if (p.tr_vn) snapshot<T>(p, gm.msg, p.tr_vn + (f * p.l_max + n_snap) * p.E, tid, true);

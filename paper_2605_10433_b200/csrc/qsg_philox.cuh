@@ -35,6 +35,8 @@ __device__ __forceinline__ U64x4 philox4x64_10(uint64_t c0, uint64_t key0, uint6
 }
 
 // Inverse CDF of channel.py:70-75 (later masks override earlier ones).
+// (The branch-free form n ^ (n >> 1), n = #thresholds <= k, measured 2.5%
+// slower at p = 0.02.)
 __device__ __forceinline__ uint8_t pauli_from_word(uint64_t w, uint64_t kx, uint64_t ky, uint64_t kz)
 {
     const uint64_t k = w >> 11;
