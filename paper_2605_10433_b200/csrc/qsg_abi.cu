@@ -310,8 +310,8 @@ int compile_layout(qsg_graph *g, int32_t n, int32_t m, const int64_t *cn_ptr, co
     g->off_synw = (uint32_t)off; off += (size_t)8 * g->nw;
     g->off_resw = (uint32_t)off; off += (size_t)8 * g->nw;
     off = (off + 7) / 8 * 8;
-    // scratch: group_sum slots, the frame index (8 B), the per-group tallies (16 B)
-    g->off_scratch = (uint32_t)off; off += 2 * (T / 32) * 4 + 8;
+    // scratch: group_sum slots, the frame index (8 B), the per-group tallies (24 B)
+    g->off_scratch = (uint32_t)off; off += 2 * (T / 32) * 4 + 8 + 24;
     g->group_bytes = (uint32_t)((off + 15) / 16 * 16);
     return QSG_OK;
 }

@@ -660,7 +660,11 @@ __device__ __forceinline__ void cn_phase(const KParams &p, const GroupMem &gm, u
             const uint32_t s1 = gm.synw[wd1] >> bit, r1 = gm.resw[wd1] >> bit;
             uint32_t ad0[D], ad1[D];
             float v0[D], v1[D];
+#ifdef QSG_BP4_PAIR
+            if constexpr (false) {
+#else
             if constexpr (BP4) {
+#endif
                 // one check at a time: the product-form update is long enough
                 // to hide its loads, and the second check's 2D live values
                 // would push the kernel past its register budget
@@ -1070,10 +1074,16 @@ __device__ __forceinline__ uint8_t ehat_of(const KParams &p, const GroupMem &gm,
 // for W = 8, whose 12 / 16 fp32 messages per qubit slot limit the frames per
 // SM by shared memory anyway (<= 18 / 13) -- under the 640 bound those
 // kernels spilled (BASELINE config 4).
-constexpr int max_threads(int W) { return W == 8 ? 384 : (W == 6 ? 512 : 640); }
+#ifndef QSG_BP4_THREADS
+#define QSG_BP4_THREADS 512
+#endif
+constexpr int max_threads(int W, bool BP4)
+{
+    return W == 8 ? 384 : (W == 6 ? 512 : (BP4 ? QSG_BP4_THREADS : 640));
+}
 
 template <int W, int T, bool BP4, bool ADD, int NP>
-__global__ void __launch_bounds__(max_threads(W)) decode_kernel(const KParams p)
+__global__ void __launch_bounds__(max_threads(W, BP4)) decode_kernel(const KParams p)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     // ---- per-CTA copy of the graph tables ----
@@ -1108,10 +1118,14 @@ __global__ void __launch_bounds__(max_threads(W)) decode_kernel(const KParams p)
     gm.resw = reinterpret_cast<uint32_t *>(gbase + p.off_resw);
     int *scratch = reinterpret_cast<int *>(gbase + p.off_scratch);  // 2*(T/32) ints
     long long *fslot = reinterpret_cast<long long *>(scratch + 2 * (T / 32));
+    // per-group tallies {frames, failures, sum iterations}, kept by thread 0
+    // in shared memory (three 64-bit registers live across the whole frame
+    // loop cost the BP4 kernels their last spills)
+    unsigned long long *tally = reinterpret_cast<unsigned long long *>(fslot + 1);
 
     const int n = p.n, m = p.m, np_ = p.n_pad;
     const int msg_words = p.dv_max * np_;
-    long long c_frames = 0, c_fail = 0, c_iters = 0;
+    if (tid == 0) tally[0] = tally[1] = tally[2] = 0ull;
 
     // hard decision with all-zero check messages: argmin(0, L0, L0, L0)
     const uint32_t hd0 = hard_decision(p.l0, p.l0, p.l0);
@@ -1295,18 +1309,18 @@ __global__ void __launch_bounds__(max_threads(W)) decode_kernel(const KParams p)
             if (p.out_flag) p.out_flag[f] = (uint8_t)(p.sample ? !success : success);
             if (p.out_iters) p.out_iters[f] = iters;
             if (p.tr_counts) { p.tr_counts[2 * f] = n_gamma; p.tr_counts[2 * f + 1] = n_snap; }
+            tally[0] += 1ull;
+            tally[1] += (unsigned long long)!success;
+            tally[2] += (unsigned long long)iters;
         }
-        ++c_frames;
-        c_fail += !success;
-        c_iters += iters;
         group_sync<T>(g);  // group memory reuse by the next frame
     }
-    if (p.counters && tid == 0 && c_frames) {
-        atomicAdd((unsigned long long *)&p.counters[0], (unsigned long long)c_frames);
-        atomicAdd((unsigned long long *)&p.counters[1], (unsigned long long)c_fail);
-        atomicAdd((unsigned long long *)&p.counters[2], (unsigned long long)c_iters);
-        atomicAdd((unsigned long long *)&p.counters[3],
-                  (unsigned long long)(p.E * (c_iters - c_frames)));
+    if (p.counters && tid == 0 && tally[0]) {
+        const unsigned long long c_frames = tally[0], c_iters = tally[2];
+        atomicAdd((unsigned long long *)&p.counters[0], c_frames);
+        atomicAdd((unsigned long long *)&p.counters[1], tally[1]);
+        atomicAdd((unsigned long long *)&p.counters[2], c_iters);
+        atomicAdd((unsigned long long *)&p.counters[3], (unsigned long long)p.E * (c_iters - c_frames));
     }
 }
 

@@ -152,40 +152,56 @@ __device__ __forceinline__ F2 bp4_out2(F2 EOa, F2 EOb)
 }
 
 // BP4 product-form magnitudes (qsg_math.cuh bp4_mags) for a check of
-// compile-time degree D (even): exponentials on edge pairs, the prefix and
-// suffix recurrences side by side on FFMA2 (prefix in the low half, suffix
-// in the high half), the per-edge merge as an FMUL2 + FFMA2 (E, O) pair, and
-// the reciprocal, ratio and logarithm of two edges as pairs.  Each half performs exactly the scalar
-// recipe's operations (bit-identical).
+// compile-time degree D (even), laid out so that every FFMA2 operand is a
+// register pair as produced, its swapped halves or one broadcast register
+// (all free operand forms on sm_100; packing two values from different pairs
+// costs a move, which lands on the FMA pipe this kernel is bound by):
+//   prefix pair PA_j = (A_j, B_j):  PA_{j+1} = fma(s_j, swap(PA_j), PA_j)
+//   suffix pair SC_e = (C_e, D_e):  SC_{e-1} = fma(s_e, swap(SC_e), SC_e)
+//   merge  (E_e, O_e) = fma(A_e, SC_e, B_e * swap(SC_e))
+// (halves: A + s B, B + s A / C + s D, D + s C / A C + B D, A D + B C -- the
+// scalar recipe's operations, bit-identical).  Exponentials run on edge
+// pairs, the ratio E * rcp(O) as two scalar products, and the reciprocal and
+// logarithm of two edges as pairs.  Edges are finished as soon as their
+// prefix and suffix exist (two per step from the middle), which keeps few
+// partial products live.
+__device__ __forceinline__ F2 swp(F2 a) { return pk(hi(a), lo(a)); }
+
+__device__ __forceinline__ F2 bp4_merge(F2 PA, F2 SC)
+{
+    return fma2(bc(lo(PA)), SC, mul2(bc(hi(PA)), swp(SC)));  // (E, O)
+}
+
+// magnitudes of two edges from their (E, O) pairs
+__device__ __forceinline__ F2 bp4_out2s(F2 EOa, F2 EOb)
+{
+    const F2 y = rcp3_2(pk(fmaxf(hi(EOa), 1e-30f), fmaxf(hi(EOb), 1e-30f)));
+    const F2 L = log_pos2(pk(lo(EOa) * lo(y), lo(EOb) * hi(y)));
+    return pk(fminf(fmaxf(lo(L), kPhi50), kPhiTiny), fminf(fmaxf(hi(L), kPhi50), kPhiTiny));
+}
+
 template <int D>
 __device__ __forceinline__ void bp4_mags_fixed(const float (&x)[D], float (&mag)[D])
 {
     static_assert(D % 2 == 0, "paired exponentials need an even degree");
-    float s[D], A[D], B[D], C[D], Dd[D];
+    float s[D];
 #pragma unroll
     for (int k = 0; k < D; k += 2) {
         const F2 e = exp_neg2(pk(-x[k], -x[k + 1]));
         s[k] = lo(e); s[k + 1] = hi(e);
     }
-    A[0] = 1.0f; B[0] = 0.0f; C[D - 1] = 1.0f; Dd[D - 1] = 0.0f;
-    F2 P = bc(1.0f), Q = bc(0.0f);  // (A_j, C_{D-1-j}), (B_j, D_{D-1-j})
-    // edges are merged as soon as their prefix (step e - 1) and suffix
-    // (step D - 2 - e) exist -- two per step from step D/2 - 1, which keeps
-    // fewer partial products live -- and finished as a pair
-    auto merge = [&](int e) {
-        const F2 t = mul2(bc(B[e]), pk(Dd[e], C[e]));            // (B D, B C)
-        return fma2(bc(A[e]), pk(C[e], Dd[e]), t);               // (E_e, O_e)
-    };
+    F2 PA[D], SC[D];
+    PA[0] = pk(1.0f, 0.0f);
+    SC[D - 1] = pk(1.0f, 0.0f);
 #pragma unroll
     for (int j = 0; j + 1 < D; ++j) {
-        const F2 S = pk(s[j], s[D - 1 - j]);
-        const F2 Pn = fma2(S, Q, P), Qn = fma2(S, P, Q);
-        P = Pn; Q = Qn;
-        A[j + 1] = lo(P); B[j + 1] = lo(Q); C[D - 2 - j] = hi(P); Dd[D - 2 - j] = hi(Q);
+        PA[j + 1] = fma2(bc(s[j]), swp(PA[j]), PA[j]);
+        SC[D - 2 - j] = fma2(bc(s[D - 1 - j]), swp(SC[D - 1 - j]), SC[D - 1 - j]);
         if (D - 2 - j < j + 1) {  // new edges D - 2 - j and j + 1
-            const F2 m = bp4_out2(merge(D - 2 - j), merge(j + 1));
-            mag[D - 2 - j] = lo(m);
-            mag[j + 1] = hi(m);
+            const int a = D - 2 - j, b = j + 1;
+            const F2 m = bp4_out2s(bp4_merge(PA[a], SC[a]), bp4_merge(PA[b], SC[b]));
+            mag[a] = lo(m);
+            mag[b] = hi(m);
         }
     }
 }

@@ -130,6 +130,10 @@ def harness():
         "small_ms_cap": (small, sweep("gb-10-2", "ms", (0.001,), 5, l_max=8, target_failures=500, max_frames=64), 0.001),
         "small_ms_fixed_prior": (small, sweep("gb-10-2", "ms", (0.2,), 8, l_max=4, target_failures=30,
                                              epsilon0_mode="fixed", epsilon0=0.1), 0.2),
+        # fixed prior where fp32 and fp64 decide every frame alike (the MS
+        # case above is tie-dominated: DESIGN.md section 8, tests/test_gpu_dropin.py)
+        "small_sagms_fixed_prior": (small, sweep("gb-10-2", "sagms", (0.2,), 8, l_max=4, target_failures=30,
+                                                epsilon0_mode="fixed", epsilon0=0.1), 0.2),
     }
     for name, (H, cfg, eps) in cases.items():
         p = run_point(H, tanner_graph(H), cfg, eps)
