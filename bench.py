@@ -52,6 +52,10 @@ METRIC = "decoded frames/s and CN-edge updates/s per GPU & 8×B200 (% roofline),
 # Algorithmic ops per CN-edge update: ALU + MUFU-class
 # ops of the reference algorithm, the numerator of roofline.achieved.
 OPS_PER_EDGE = {"sagms": 30.3 + 4, "sms": 30.0 + 4, "ms": 29.0 + 4, "bp4": 34.1 + 10}
+# FP32-pipe lane operations per BP4 CN-edge update of the fp32 recipe
+# (check side 40.6: exponential 11, prefix/suffix 3.6, merge 4, reciprocal 7,
+# ratio 1, logarithm 14; qubit side 10.8 per edge); DESIGN.md section 4
+BP4_FP32_OPS = 51.4
 
 
 # BASELINE configs[4] (strong scaling): GbSpec args, p values, total frames per point
@@ -344,23 +348,39 @@ def run_ours(args, rank, world, local_rank):
     f_sm = (clocks["sm_mhz"] or 1965.0) * 1e6
     peak = dg_sms() * 128 * f_sm
     achieved = ops / (ms_mins / 1e3)
+    # hardware counters of the committed ncu capture, used only when it was
+    # taken on THIS build (qsg_build_id(): hash of the kernel sources and flags)
     traffic = issue_busy = None
+    bp4_hw = {}
+    tj = {}
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
             tj = json.load(fh)
-            traffic = tj.get("bytes_per_launch")
-            issue_busy = tj.get("issue_slots_busy")
+    build_id = P._native.lib().qsg_build_id().decode()
+    ncu_match = tj.get("build_id") == build_id
+    if ncu_match:
+        traffic = tj.get("bytes_per_launch")
+        issue_busy = tj.get("issue_slots_busy")
+        bp4_hw = tj.get("bp4", {})
     share = ms_mins / (sum(l[0] for l in launch_ms) / args.steps)
-    # the BP4 launches (the rest of the step), against the same issue roof
-    # and against SURVEY 8(d)'s MUFU-class roof for BP4 (10 of its 44.1 ops)
+    # the BP4 launches (the rest of the step): against the same issue roof
+    # (SURVEY 8(d)'s 44.1 ops per edge) and against the pipe that binds them,
+    # the FP32 pipe (ncu: math-pipe throttle is their top stall): the fp32
+    # recipe performs BP4_FP32_OPS FP32-pipe lane operations per CN-edge
+    # update, peak 128 per SM per clock
     bp4s = [k for k, (name, _, _) in enumerate(points) if name == "bp4"]
     ms_bp4 = sum(launch_ms[k][0] for k in bp4s) / args.steps
     upd_bp4 = sum(cnt[k, 3] / world for k in bp4s)
-    bp4_line = {"achieved": upd_bp4 * OPS_PER_EDGE["bp4"] / (ms_bp4 / 1e3) / 1e9, "peak": peak / 1e9,
-                "unit": "Gop/s", "frac": upd_bp4 * OPS_PER_EDGE["bp4"] / (ms_bp4 / 1e3) / peak,
-                "cn_edge_updates_per_s": upd_bp4 / (ms_bp4 / 1e3),
-                "frac_of_mufu_roof": (upd_bp4 / (ms_bp4 / 1e3)) / (dg_sms() * 16 * f_sm / 10),
+    bp4_rate = upd_bp4 / (ms_bp4 / 1e3)
+    bp4_line = {"achieved": bp4_rate * OPS_PER_EDGE["bp4"] / 1e9, "peak": peak / 1e9,
+                "unit": "Gop/s", "frac": bp4_rate * OPS_PER_EDGE["bp4"] / peak,
+                "cn_edge_updates_per_s": bp4_rate,
+                "fp32_pipe": {"bound": "fp32 pipe", "ops_per_cn_edge_update": BP4_FP32_OPS,
+                              "achieved": bp4_rate * BP4_FP32_OPS / 1e9, "peak": peak / 1e9, "unit": "Gop/s",
+                              "frac": bp4_rate * BP4_FP32_OPS / peak,
+                              "ncu_fma_pipe_cycles_active": bp4_hw.get("fma_pipe_cycles_active"),
+                              "ncu_issue_slots_busy": bp4_hw.get("issue_slots_busy")},
                 "kernel": "qsg::decode_kernel<5,32,true,false,256> (BP4, marginal VN)",
                 "share_of_step": ms_bp4 / (sum(l[0] for l in launch_ms) / args.steps)}
 
@@ -401,7 +421,8 @@ def run_ours(args, rank, world, local_rank):
                      "ops_per_cn_edge_update": "SURVEY.md 8(d): SAGMS 34.3, SMS 34.0",
                      "peak_basis": "148 SMs x 128 lane-instr/clk x measured median SM clock",
                      "share_of_step": share,
-                     "ncu_issue_slots_busy": issue_busy},
+                     "ncu_issue_slots_busy": issue_busy,
+                     "ncu_build_id": tj.get("build_id"), "build_id": build_id, "ncu_build_match": ncu_match},
         "roofline_bp4": bp4_line,
         "e2e": {"value": e2e_value, "unit": "frames/s", "h2d_bytes_per_step": int(e2e_h2d),
                 "d2h_bytes_per_step": int(e2e_d2h),

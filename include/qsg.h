@@ -158,6 +158,11 @@ int qsg_syndromes_of(const qsg_graph *g, const uint8_t *e_dev, int64_t B, uint8_
 /* Thread-local description of the last failure (never NULL). */
 const char *qsg_last_error(void);
 int qsg_abi_version(void);
+/* Hash of the kernel sources and build flags the library was compiled from
+ * (16 hex digits).  Not a reference interface: profiles/ncu_traffic.json
+ * records the id its ncu capture was taken on, and bench.py refuses
+ * hardware counters from a different build. */
+const char *qsg_build_id(void);
 
 #ifdef __cplusplus
 }

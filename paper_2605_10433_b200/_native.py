@@ -29,6 +29,7 @@ EXPORTS = (
     "qsg_graph_export", "qsg_decode_syndromes", "qsg_decode_syndromes_packed", "qsg_decode_frames",
     "qsg_sample_errors",
     "qsg_syndromes_of", "qsg_graph_check_commute", "qsg_last_error", "qsg_abi_version",
+    "qsg_build_id",
 )
 
 
@@ -89,6 +90,8 @@ def lib():
         L.qsg_last_error.restype = C.c_char_p
         L.qsg_last_error.argtypes = []
         L.qsg_abi_version.argtypes = []
+        L.qsg_build_id.restype = C.c_char_p
+        L.qsg_build_id.argtypes = []
         _lib = L
     return _lib
 

@@ -607,6 +607,11 @@ extern "C" {
 
 int qsg_abi_version(void) { return QSG_ABI_VERSION; }
 
+#ifndef QSG_BUILD_ID
+#define QSG_BUILD_ID "unknown"
+#endif
+const char *qsg_build_id(void) { return QSG_BUILD_ID; }
+
 const char *qsg_last_error(void) { return g_last_error.c_str(); }
 
 int qsg_graph_create_csr(int32_t n, int32_t m, const int64_t *cn_ptr, const int64_t *edge_vn,

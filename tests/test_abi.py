@@ -45,9 +45,31 @@ def test_kernels_are_sm100a():
     from paper_2605_10433_b200 import _native
     out = subprocess.run(["cuobjdump", "--list-elf", _native.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
-    sass = subprocess.run(["cuobjdump", "-sass", "-fun", "decode_kernel", _native.LIB_PATH],
-                          capture_output=True, text=True).stdout
-    assert "FFMA" in sass or len(sass) > 0
+    sass = subprocess.run(["cuobjdump", "-sass", _native.LIB_PATH], capture_output=True, text=True).stdout
+    funcs = {}
+    cur = None
+    for ln in sass.splitlines():
+        if "Function : " in ln:
+            cur = ln.split("Function : ")[1].strip()
+            funcs[cur] = []
+        elif cur:
+            funcs[cur].append(ln)
+    # the BASELINE configs[1] kernels (W = 5, one warp per frame, n_pad 256)
+    ms = "\n".join(funcs["_ZN3qsg13decode_kernelILi5ELi32ELb0ELb0ELi256EEEvNS_7KParamsE"])
+    bp4 = "\n".join(funcs["_ZN3qsg13decode_kernelILi5ELi32ELb1ELb0ELi256EEEvNS_7KParamsE"])
+    # min-sum: min1/min2 with the sign product riding on min (FMNMX), paired
+    # qubit factors (FFMA2), frame queue (ATOMG), ballot-packed bitmaps (VOTE)
+    for op in ("FMNMX", "FFMA2", "ATOMG", "VOTE", "LDS.U16", "SHFL"):
+        assert op in ms, op
+    # BP4: product-form recipe on FFMA2 / FMUL2.  Neither kernel uses the
+    # hardware approximations MUFU.EX2 / LG2 (the fp32 recipes must be
+    # reproducible by the CPU oracle; the only MUFU is the RCP seed of integer /
+    # double divisions outside the recipes), and neither spills
+    for op in ("FFMA2", "FMUL2"):
+        assert op in bp4, op
+    for k in (ms, bp4):
+        assert "MUFU.EX2" not in k and "MUFU.LG2" not in k
+        assert "STL" not in k and "LDL" not in k
 
 
 @pytest.mark.parametrize("spec,kind", [(TOY, 0), (SMALL, 0), (GB126, 5), (GB254, 5), (GB1022, 5),

@@ -24,6 +24,7 @@ if has launch; then
 fi
 if has ncu; then
   CODE=${CODE:-254}; VAR=${VAR:-sagms}; P=${P:-0.08}
+  python -c "import sys; sys.path.insert(0, '.'); from paper_2605_10433_b200 import _native; print(_native.lib().qsg_build_id().decode())" > $O/build_id_$TAG.txt
   PCMD="python tools/perf_probe.py $CODE $VAR $P"
   FRAMES=131072 timeout 300 $PCMD > $O/plain_probe_$TAG.log 2>&1 && \
     FRAMES=131072 timeout 1200 ncu --set full --clock-control none --import-source on \
