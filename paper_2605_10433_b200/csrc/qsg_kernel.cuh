@@ -1069,21 +1069,30 @@ __device__ __forceinline__ uint8_t ehat_of(const KParams &p, const GroupMem &gm,
     }
 }
 
-// Threads-per-CTA bound per W, which sets the register budget: 640 (96
-// registers, 20 warps per SM) for W <= 5; 512 (128) for W = 6 and 384 (168)
-// for W = 8, whose 12 / 16 fp32 messages per qubit slot limit the frames per
-// SM by shared memory anyway (<= 18 / 13) -- under the 640 bound those
-// kernels spilled (BASELINE config 4).
+// Threads-per-CTA bound per kernel, which sets its register budget (the
+// register file is 16K 32-bit registers per SM sub-partition, so a bound of
+// 5 warps per sub-partition gives 96 registers, 4 warps 128, 3 warps 168):
+//  * bicycle W <= 5 min-sum: 640 (96 registers, 20 one-warp frames per SM,
+//    which is also the shared-memory limit at l = 127);
+//  * bicycle BP4 (W <= 5): 512 (128; its product-form check update needs a
+//    few more than 96 -- spill-free, and +1-2% at p >= 0.06 despite 16
+//    frames per SM instead of 20);
+//  * W = 6 / 8: 512 / 384, whose 12 / 16 fp32 messages per qubit slot limit
+//    the frames per SM by shared memory anyway (<= 18 / 13);
+//  * generic kernels with degree bound >= 12: 256, their register arrays
+//    (messages, addresses and, for BP4, prefix products per edge) need up to
+//    the 255-register maximum; <= 8: 640.
 #ifndef QSG_BP4_THREADS
 #define QSG_BP4_THREADS 512
 #endif
-constexpr int max_threads(int W, bool BP4)
+constexpr int max_threads(int W, bool BP4, int NP)
 {
+    if (W == 0) return NP >= 12 ? 256 : 640;
     return W == 8 ? 384 : (W == 6 ? 512 : (BP4 ? QSG_BP4_THREADS : 640));
 }
 
 template <int W, int T, bool BP4, bool ADD, int NP>
-__global__ void __launch_bounds__(max_threads(W, BP4)) decode_kernel(const KParams p)
+__global__ void __launch_bounds__(max_threads(W, BP4, NP), W == 0 ? 1 : 0) decode_kernel(const KParams p)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     // ---- per-CTA copy of the graph tables ----

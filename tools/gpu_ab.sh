@@ -1,7 +1,12 @@
-cd $GRAFT_REPO_ROOT
+#!/bin/bash
+# A/B of library builds in abl/ against the in-tree build (dev tool).
+# Usage: LIBS="abl/a.so ..." CASES="254:sagms,bp4:0.02,0.1 1022:sagms:0.03" tools/gpu_ab.sh
+cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/gputest_r02b.log 2>&1; echo "tests rc=$?"; tail -5 gpurun_out/gputest_r02b.log
-LIBS="abl/b512.so paper_2605_10433_b200/libqsg.so" bash tools/ab3.sh 254 bp4 0.02,0.06,0.08,0.1 > gpurun_out/ab3.log 2>&1
-LIBS="abl/b512.so paper_2605_10433_b200/libqsg.so" bash tools/ab3.sh 1022,rgb127w8 bp4 0.04,0.08 >> gpurun_out/ab3.log 2>&1
-python tools/ab_table.py gpurun_out/ab3.log
-TAG=bp4_r02b VAR=bp4 P=0.1 STEPS=ncu bash tools/gpu_session.sh
+OUT=gpurun_out/${ABTAG:-ab}.log
+: > $OUT
+for c in $CASES; do
+  IFS=: read code dec ps <<< "$c"
+  LIBS="$LIBS paper_2605_10433_b200/libqsg.so" bash tools/ab3.sh $code $dec $ps >> $OUT 2>&1
+done
+python tools/ab_table.py $OUT
