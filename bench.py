@@ -520,9 +520,22 @@ def strong_config5(args, rank, world, dev, l2):
                     if rep:
                         shard_ms[r][k] = e0.elapsed_time(e1)
         per_rank = [sum(x) for x in shard_ms]
+        # and per point: t(2^22 frames) / (8 x slowest 2^19-frame shard)
+        full_ms = []
+        for k, (_, dg, p) in enumerate(pts):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            P.decode_frames_device(dg, cfg, p, p, SEED, 0, C5_FRAMES, counters=None, want_frames=False)
+            e1.record()
+            torch.cuda.synchronize()
+            full_ms.append(e0.elapsed_time(e1))
         out["proxy_8way"] = {
             "shard_ms_max_over_8": max(per_rank), "shard_ms_min_over_8": min(per_rank),
             "efficiency": ms / (8 * max(per_rank)),
+            "per_point": [{"code": cname, "p": p, "full_ms": full_ms[k],
+                           "shard_ms_max": max(shard_ms[r][k] for r in range(8)),
+                           "efficiency": full_ms[k] / (8 * max(shard_ms[r][k] for r in range(8)))}
+                          for k, (cname, _, p) in enumerate(pts)],
             "note": "t(2^22 frames on 1 GPU) / (8 x slowest 1/8 shard timed alone): the strong-scaling "
                     "efficiency an 8-GPU run would reach with zero collective cost"}
     return out

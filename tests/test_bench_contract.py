@@ -77,3 +77,26 @@ def test_gpu_arm_two_ranks_on_one_gpu():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["frames_per_step"] == 2 * 35 * 16384
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and "cpu_baseline" not in d
+
+
+@pytest.mark.gpu
+def test_gpu_arm_self_spawns_ranks():
+    """`python bench.py --gpus 2` without a torchrun environment re-executes
+    itself under torch.distributed.run with 2 local ranks (the driver may
+    launch either way).  On this one-GPU pool both ranks share cuda:0 and
+    use gloo; the line reports both ranks and the strong-scaling config-5
+    leg sharded over them."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR",
+                                                              "MASTER_PORT")}
+    env.update(QSG_BENCH_FRAMES="16384", QSG_BENCH_C5_FRAMES="65536", QSG_BENCH_BACKEND="gloo")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1",
+                          "--warmup", "3", "--no-cpu"], capture_output=True, text=True, env=env, timeout=900,
+                         cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["frames_per_step"] == 2 * 35 * 16384
+    c5 = d["strong_config5"]
+    assert c5["n_gpus"] == 2 and c5["scaling"] == "strong" and c5["frames_per_step"] == 4 * 65536
+    assert all(pt["frames"] == 65536 for pt in c5["points"])
