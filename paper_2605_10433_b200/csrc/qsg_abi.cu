@@ -426,6 +426,7 @@ int launch_decode(qsg_graph *g, const qsg_decoder_cfg *cfg, qsg::KParams &p, cud
     }
     QSG_CUDA(cudaMemsetAsync(queue, 0, sizeof(unsigned long long), st));
     p.queue = queue;
+    p.zero = 0;  // queue_fetch: opaque zero offset (keeps the frame-queue atomic un-aggregated)
     p.groups = lc.groups;
     void *args[] = {&p};
     cudaError_t err = cudaLaunchKernel(fn, dim3(grid), dim3(lc.groups * g->threads), args, lc.smem, st);

@@ -90,6 +90,7 @@ struct KParams {
     uint8_t *out_ehat;
     int64_t *counters;
     unsigned long long *queue;
+    int32_t zero;  // always 0 (queue_fetch)
     // traces (syndrome mode)
     int32_t *tr_unsat;
     float *tr_vn, *tr_cn;
@@ -99,6 +100,18 @@ struct KParams {
     uint32_t tab_bytes, group_bytes;
     uint32_t off_ehat, off_bits, off_synw, off_resw, off_scratch;
 };
+
+// Frame-queue fetch by one thread.  On a warp-uniform address ptxas turns
+// any atomic add into a warp-aggregated one (leader vote, popc, and a
+// shuffle of the result right after the atomic), which stalls the warp for
+// the atomic's round trip at every frame start.  The address is therefore
+// offset by threadIdx.x * KParams::zero (0 at run time, opaque to the
+// compiler): a plain ATOMG whose result register is first read at the NEXT
+// frame start, so the round trip overlaps the current frame.
+__device__ __forceinline__ unsigned long long queue_fetch(unsigned long long *q, int32_t zero)
+{
+    return atomicAdd(q + threadIdx.x * (uint32_t)zero, 1ull);
+}
 
 // ---- optional-value arithmetic for compile-time masked reductions ---------
 // np.add.reduceat over cv * anti_mask keeps the masked (+-0) entries in
@@ -1150,7 +1163,7 @@ __global__ void __launch_bounds__(max_threads(W, BP4, NP), W == 0 ? 1 : 0) decod
     // current one is known, so the global atomic's round trip overlaps the
     // current frame's decode instead of stalling the group between frames
     long long f_next = 0;
-    if (tid == 0) f_next = (long long)atomicAdd(p.queue, 1ull);
+    if (tid == 0) f_next = (long long)queue_fetch(p.queue, p.zero);
     while (true) {
         long long f;
         if constexpr (T == 32) {
@@ -1162,7 +1175,7 @@ __global__ void __launch_bounds__(max_threads(W, BP4, NP), W == 0 ? 1 : 0) decod
             group_sync<T>(g);
         }
         if (f >= p.count) break;
-        if (tid == 0) f_next = (long long)atomicAdd(p.queue, 1ull);
+        if (tid == 0) f_next = (long long)queue_fetch(p.queue, p.zero);
 
         // ---- frame input: observed syndrome ----
         uint32_t syn_bits = 0;
