@@ -53,9 +53,10 @@ METRIC = "decoded frames/s and CN-edge updates/s per GPU & 8×B200 (% roofline),
 # ops of the reference algorithm, the numerator of roofline.achieved.
 OPS_PER_EDGE = {"sagms": 30.3 + 4, "sms": 30.0 + 4, "ms": 29.0 + 4, "bp4": 34.1 + 10}
 # FP32-pipe lane operations per BP4 CN-edge update of the fp32 recipe
-# (check side 40.6: exponential 11, prefix/suffix 3.6, merge 4, reciprocal 7,
-# ratio 1, logarithm 14; qubit side 10.8 per edge); DESIGN.md section 4
-BP4_FP32_OPS = 51.4
+# (check side 36.6: exponential 11, prefix/suffix 3.6, merge 4, reciprocal 3
+# (its MUFU seed runs on the XU pipe), ratio 1, logarithm 14; qubit side 10.8
+# per edge); DESIGN.md section 5
+BP4_FP32_OPS = 47.4
 
 
 # BASELINE configs[4] (strong scaling): GbSpec args, p values, total frames per point
@@ -368,7 +369,7 @@ def run_ours(args, rank, world, local_rank):
     # (SURVEY 8(d)'s 44.1 ops per edge) and against the pipe that binds them,
     # the FP32 pipe (ncu: math-pipe throttle is their top stall): the fp32
     # recipe performs BP4_FP32_OPS FP32-pipe lane operations per CN-edge
-    # update (DESIGN.md section 4), peak 128 per SM per clock
+    # update (DESIGN.md section 5), peak 128 per SM per clock
     bp4s = [k for k, (name, _, _) in enumerate(points) if name == "bp4"]
     ms_bp4 = sum(launch_ms[k][0] for k in bp4s) / args.steps
     upd_bp4 = sum(cnt[k, 3] / world for k in bp4s)

@@ -133,20 +133,20 @@ __device__ __forceinline__ F2 vn_F2(float y0, float y1, F2 kapc2)
     return fma2(sub2(bc(0.0f), q), log1p_01_poly2(q), log_pos2(A));
 }
 
-// rcp3 on both halves (o > 0).
-__device__ __forceinline__ F2 rcp3_2(F2 o)
+// rcp_rn on both halves: two MUFU.RCP seeds, the Newton step on FFMA2.
+__device__ __forceinline__ F2 rcp_rn2(F2 o)
 {
-    F2 y = pk(u2f(0x7ef311c3u - f2u(lo(o))), u2f(0x7ef311c3u - f2u(hi(o))));
-    const F2 no = sub2(bc(0.0f), o);  // -o, exact
-#pragma unroll
-    for (int i = 0; i < 3; ++i) y = fma2(y, fma2(no, y, bc(1.0f)), y);
-    return y;
+    float y0, y1;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y0) : "f"(lo(o)));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y1) : "f"(hi(o)));
+    const F2 y = pk(y0, y1);
+    return fma2(y, fma2(sub2(bc(0.0f), o), y, bc(1.0f)), y);  // 0 - o = -o exactly
 }
 
 // BP4 magnitudes of two edges from their (E, O) pairs.
 __device__ __forceinline__ F2 bp4_out2(F2 EOa, F2 EOb)
 {
-    const F2 y = rcp3_2(pk(fmaxf(hi(EOa), 1e-30f), fmaxf(hi(EOb), 1e-30f)));
+    const F2 y = rcp_rn2(pk(fmaxf(hi(EOa), 1e-30f), fmaxf(hi(EOb), 1e-30f)));
     const F2 L = log_pos2(mul2(pk(lo(EOa), lo(EOb)), y));
     return pk(fminf(fmaxf(lo(L), kPhi50), kPhiTiny), fminf(fmaxf(hi(L), kPhi50), kPhiTiny));
 }
@@ -175,7 +175,7 @@ __device__ __forceinline__ F2 bp4_merge(F2 PA, F2 SC)
 // magnitudes of two edges from their (E, O) pairs
 __device__ __forceinline__ F2 bp4_out2s(F2 EOa, F2 EOb)
 {
-    const F2 y = rcp3_2(pk(fmaxf(hi(EOa), 1e-30f), fmaxf(hi(EOb), 1e-30f)));
+    const F2 y = rcp_rn2(pk(fmaxf(hi(EOa), 1e-30f), fmaxf(hi(EOb), 1e-30f)));
     const F2 L = log_pos2(pk(lo(EOa) * lo(y), lo(EOb) * hi(y)));
     return pk(fminf(fmaxf(lo(L), kPhi50), kPhiTiny), fminf(fmaxf(hi(L), kPhi50), kPhiTiny));
 }

@@ -265,7 +265,10 @@ def test_unplanned_syndrome_shapes_bit_exact(P, oracle, monkeypatch, ell, w, thr
 def test_paired_recipes_equal_scalar_on_device(tmp_path):
     """tools/pair_check.cu: every paired (FFMA2/FADD2/FMUL2) recipe of
     qsg_math2.cuh equals two calls of its scalar qsg_math.cuh counterpart
-    bit for bit on 5e5 argument pairs per function, on the device."""
+    bit for bit on 5e5 argument pairs per function, on the device; and the
+    BP4 reciprocal rcp_rn (MUFU seed + one Newton step) equals the IEEE
+    division 1/o -- what the CPU oracle computes -- for every float in
+    [2^-100, 2^34)."""
     import subprocess
     root = Path(__file__).resolve().parents[1]
     exe = tmp_path / "pair_check"
@@ -273,6 +276,7 @@ def test_paired_recipes_equal_scalar_on_device(tmp_path):
                     "-o", str(exe), str(root / "tools" / "pair_check.cu")], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert "RECIPE_MISMATCHES 0" in out.stdout, out.stdout[-2000:]
+    assert "RCP_RN_VS_DIV mismatches 0 /" in out.stdout, out.stdout[-2000:]
     assert out.returncode == 0
 
 

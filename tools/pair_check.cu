@@ -21,7 +21,7 @@ __global__ void k(const float* x, float* o, int n, int which) {
     case 1: s0 = log1p_01(a); s1 = log1p_01(b); r = log1p_01_2(pk(a, b)); break;
     case 2: s0 = log_pos(a); s1 = log_pos(b); r = log_pos2(pk(a, b)); break;
     case 3: s0 = vn_F(a, 0.03f); s1 = vn_F(b, 0.03f); r = vn_F2(a, b, bc(0.03f)); break;
-    case 4: s0 = rcp3(a); s1 = rcp3(b); r = rcp3_2(pk(a, b)); break;
+    case 4: s0 = rcp_rn(a); s1 = rcp_rn(b); r = rcp_rn2(pk(a, b)); break;
     case 5: case 6: case 7: {  // one BP4 check (degree 10 / 10 / 6) from (a, b)
       float x[10], ms[10], mp[10];
       for (int q = 0; q < 10; ++q) x[q] = fminf(fabsf(a * (1.0f + q) - b * (3.0f - 0.7f * q)), 64.0f);
@@ -56,11 +56,20 @@ __global__ void k(const float* x, float* o, int n, int which) {
   p0 = lo(r); p1 = hi(r);
   o[4 * i] = s0; o[4 * i + 1] = s1; o[4 * i + 2] = p0; o[4 * i + 3] = p1;
 }
+__global__ void rcp_vs_div(uint32_t lo_bits, uint32_t hi_bits, unsigned long long *bad)
+{
+  unsigned long long nb = 0;
+  for (uint32_t u = lo_bits + blockIdx.x * blockDim.x + threadIdx.x; u < hi_bits; u += gridDim.x * blockDim.x) {
+    const float o = __uint_as_float(u);
+    nb += __float_as_uint(rcp_rn(o)) != __float_as_uint(__fdiv_rn(1.0f, o));
+  }
+  if (nb) atomicAdd(bad, nb);
+}
 int main() {
   const int n = 1 << 20;
   float *h = new float[n], *ho = new float[2 * n];
   float *d, *dout; cudaMalloc(&d, n * 4); cudaMalloc(&dout, 2 * n * 4);
-  const char* names[] = {"exp_neg", "log1p_01", "log_pos", "vn_F", "rcp3", "bp4_d10_ends", "bp4_d10_mid", "bp4_d6", "sub_add", "fma_imm", "mul", "add", "subc", "sub_add2"};
+  const char* names[] = {"exp_neg", "log1p_01", "log_pos", "vn_F", "rcp_rn", "bp4_d10_ends", "bp4_d10_mid", "bp4_d6", "sub_add", "fma_imm", "mul", "add", "subc", "sub_add2"};
   int recipe_bad = 0;
   for (int w = 0; w < 14; ++w) {
     srand(1);
@@ -87,5 +96,13 @@ int main() {
     if (w != 8 && w != 13) recipe_bad += bad;  // 8, 13: raw mul+add, contracted by ptxas on purpose
   }
   printf("RECIPE_MISMATCHES %d\n", recipe_bad);
-  return recipe_bad != 0;
+  // rcp_rn against the IEEE division 1/o (what the CPU oracle computes) for
+  // every float in [2^-100, 2^34): 2^23 mantissas x 134 binades
+  unsigned long long *dbad, hbad = 0;
+  cudaMalloc(&dbad, 8); cudaMemset(dbad, 0, 8);
+  const uint32_t lo_bits = (127u - 100u) << 23, hi_bits = (127u + 34u) << 23;
+  rcp_vs_div<<<4096, 256>>>(lo_bits, hi_bits, dbad);
+  cudaMemcpy(&hbad, dbad, 8, cudaMemcpyDeviceToHost);
+  printf("RCP_RN_VS_DIV mismatches %llu / %u\n", hbad, hi_bits - lo_bits);
+  return recipe_bad != 0 || hbad != 0;
 }
