@@ -227,6 +227,23 @@ __device__ __forceinline__ uint32_t hard_decision(float mX, float mZ, float mY)
     return e;
 }
 
+// The same argmin as the two bits the bicycle kernels ballot (x = code & 1,
+// z = code >> 1), straight from the compares: Z beats {I, X} iff
+// mZ < min(0, mX), Y beats all iff mY < min(0, mX, mZ), X needs mX < 0 and
+// no Z win -- two FMNMX and four FSETP whose predicates feed VOTE directly
+// (the code form costs three FSETP, two FSEL, three SEL and the bit tests).
+struct HardXZ {
+    bool x, z;
+};
+__device__ __forceinline__ HardXZ hard_xz(float mX, float mZ, float mY)
+{
+    const float t1 = fminf(0.0f, mX);
+    const bool wz = mZ < t1;
+    const bool wx = (mX < 0.0f) && !wz;
+    const bool wy = mY < fminf(t1, mZ);
+    return HardXZ{wy || wx, wy || wz};
+}
+
 // ---- group synchronisation ---------------------------------------------
 template <int T>
 __device__ __forceinline__ void group_sync(int g)
@@ -794,11 +811,56 @@ __device__ __forceinline__ void vn_load(uint32_t cs, uint32_t rowb, float (&c)[2
 }
 
 template <int W, bool ADD, int NP>
-__device__ __forceinline__ uint32_t vn_finish(uint32_t cs, uint32_t rowb, const float (&c)[2 * W], float l0,
-                                              float kapc)
+__device__ __forceinline__ HardXZ vn_finish(uint32_t cs, uint32_t rowb, const float (&c)[2 * W], float l0,
+                                            float kapc)
 {
     if constexpr (NP > 0) rowb = 4u * NP;
     constexpr int D = 2 * W;
+    if constexpr (W <= 5 && !ADD) {
+        // numpy's trees with the masks written out (segsum_c<D>): for d = 10
+        //   S_X = x0 + P, S_Z = Q + z4, tot_Y = x0 + ((P + Q) + z4),
+        //   P = (x1 + x2) + (x3 + x4), Q = (z0 + z1) + (z2 + z3);
+        // for d <= 8 the sums run left to right,
+        //   S_X = x0 + P, S_Z = Q + z_{W-1}, tot_Y = x0 + (((P + z0) + z1) ...),
+        //   P = (x1 + x2) + ..., Q = (z0 + z1) + ... (W - 1 terms each).
+        // P and Q, the two sums and the two beliefs therefore run as pairs
+        // (x_{s+1}, z_s), (x0, z_{W-1}) on FADD2 -- the same additions in
+        // half the issue slots -- and each pair is also the operand of its
+        // two outgoing messages.
+        F2 pr[W > 1 ? W - 1 : 1];
+#pragma unroll
+        for (int s = 0; s + 1 < W; ++s) pr[s] = pk(c[s + 1], c[W + s]);
+        const F2 pe = pk(c[0], c[D - 1]);
+        F2 PQ;
+        float tY;
+        if constexpr (W == 5) {
+            PQ = add2(add2(pr[0], pr[1]), add2(pr[2], pr[3]));
+            tY = c[0] + ((lo(PQ) + hi(PQ)) + c[D - 1]);
+        } else {
+            static_assert(W >= 2, "bicycle weight");
+            PQ = pr[0];
+#pragma unroll
+            for (int s = 1; s + 1 < W; ++s) PQ = add2(PQ, pr[s]);
+            float t = lo(PQ);
+#pragma unroll
+            for (int s = 0; s < W; ++s) t = t + c[W + s];
+            tY = c[0] + t;
+        }
+        const F2 S = add2(pe, PQ);      // (S_X, S_Z)
+        const F2 b2 = add2(bc(l0), S);  // (b_Z, b_X)
+        const float bY = l0 + tY;
+        const F2 v2 = add2(b2, vn_F2(hi(S), lo(S), bc(kapc)));  // (V[X], V[Z])
+        const F2 oe = sub2(v2, pe);
+        sts_a(cs, f2u(lo(oe)));  // clipped by the consumer
+        sts_a(cs + (D - 1) * rowb, f2u(hi(oe)));
+#pragma unroll
+        for (int s = 0; s + 1 < W; ++s) {
+            const F2 o = sub2(v2, pr[s]);
+            sts_a(cs + (s + 1) * rowb, f2u(lo(o)));
+            sts_a(cs + (W + s) * rowb, f2u(hi(o)));
+        }
+        return hard_xz(hi(b2), lo(b2), bY);
+    }
     OptF ox[D], oz[D], oa[D];
 #pragma unroll
     for (int s = 0; s < D; ++s) {
@@ -827,11 +889,11 @@ __device__ __forceinline__ uint32_t vn_finish(uint32_t cs, uint32_t rowb, const 
             sts_a(cs + (W + s) * rowb, f2u(hi(o2)));
         }
     }
-    return hard_decision(bX, bZ, bY);
+    return hard_xz(bX, bZ, bY);
 }
 
 template <int W, bool ADD, int NP>
-__device__ __forceinline__ uint32_t vn_update_fixed(unsigned char *col, uint32_t rowb, float l0, float kapc)
+__device__ __forceinline__ HardXZ vn_update_fixed(unsigned char *col, uint32_t rowb, float l0, float kapc)
 {
     const uint32_t cs = smem_addr(col);
     float c[2 * W];
@@ -883,7 +945,7 @@ __device__ __forceinline__ FirstTab<W> first_tab(float A, float nB, float kapc, 
 // All 32 lanes must call this (shuffles); lanes without a qubit pass
 // store = false (their loads read inside the group's area and are ignored).
 template <int W, int NP>
-__device__ __forceinline__ uint32_t vn_first_fixed(uint32_t cs, uint32_t rowb, float l0, const FirstTab<W> &t,
+__device__ __forceinline__ HardXZ vn_first_fixed(uint32_t cs, uint32_t rowb, float l0, const FirstTab<W> &t,
                                                    bool store)
 {
     if constexpr (NP > 0) rowb = 4u * NP;
@@ -912,7 +974,7 @@ __device__ __forceinline__ uint32_t vn_first_fixed(uint32_t cs, uint32_t rowb, f
             sts_a(cs + (W + s) * rowb, f2u(hi(o2)));
         }
     }
-    return hard_decision(bX, bZ, bY);
+    return hard_xz(bX, bZ, bY);
 }
 
 template <int W, int T, int NP>
@@ -930,10 +992,10 @@ __device__ __forceinline__ void vn_phase_first(const KParams &p, const GroupMem 
         const int c = c0 + (tid & 31);
         const bool ok = c < l;
         const int cc = ok ? c : c0;  // idle lanes re-read a valid column, store nothing
-        const uint32_t eL = vn_first_fixed<W, NP>(smem_addr(gm.msg + 4 * cc), rowb, l0, t, ok);
-        const uint32_t eR = vn_first_fixed<W, NP>(smem_addr(gm.msg + 4 * (l + cc)), rowb, l0, t, ok);
-        const uint32_t xl = __ballot_sync(0xffffffffu, ok && (eL & 1u)), zl = __ballot_sync(0xffffffffu, ok && (eL >> 1));
-        const uint32_t xr = __ballot_sync(0xffffffffu, ok && (eR & 1u)), zr = __ballot_sync(0xffffffffu, ok && (eR >> 1));
+        const HardXZ eL = vn_first_fixed<W, NP>(smem_addr(gm.msg + 4 * cc), rowb, l0, t, ok);
+        const HardXZ eR = vn_first_fixed<W, NP>(smem_addr(gm.msg + 4 * (l + cc)), rowb, l0, t, ok);
+        const uint32_t xl = __ballot_sync(0xffffffffu, ok && eL.x), zl = __ballot_sync(0xffffffffu, ok && eL.z);
+        const uint32_t xr = __ballot_sync(0xffffffffu, ok && eR.x), zr = __ballot_sync(0xffffffffu, ok && eR.z);
         if ((tid & 31) == 0) {
             const int wd = c0 >> 5;
             gm.bits[kXL * nw1 + wd] = xl; gm.bits[kZL * nw1 + wd] = zl;
@@ -960,14 +1022,14 @@ __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, i
 #pragma unroll 1
             for (; c0 + T + 31 < l; c0 += 2 * T) {
                 const int c = c0 + (tid & 31);
-                const uint32_t a0 = vn_update_fixed<W, ADD, NP>(msg + 4 * c, rowb, l0, kapc);
-                const uint32_t a1 = vn_update_fixed<W, ADD, NP>(msg + 4 * (l + c), rowb, l0, kapc);
-                const uint32_t b0 = vn_update_fixed<W, ADD, NP>(msg + 4 * (c + T), rowb, l0, kapc);
-                const uint32_t b1 = vn_update_fixed<W, ADD, NP>(msg + 4 * (l + c + T), rowb, l0, kapc);
-                const uint32_t xl = __ballot_sync(0xffffffffu, a0 & 1u), zl = __ballot_sync(0xffffffffu, a0 >> 1);
-                const uint32_t xr = __ballot_sync(0xffffffffu, a1 & 1u), zr = __ballot_sync(0xffffffffu, a1 >> 1);
-                const uint32_t xl2 = __ballot_sync(0xffffffffu, b0 & 1u), zl2 = __ballot_sync(0xffffffffu, b0 >> 1);
-                const uint32_t xr2 = __ballot_sync(0xffffffffu, b1 & 1u), zr2 = __ballot_sync(0xffffffffu, b1 >> 1);
+                const HardXZ a0 = vn_update_fixed<W, ADD, NP>(msg + 4 * c, rowb, l0, kapc);
+                const HardXZ a1 = vn_update_fixed<W, ADD, NP>(msg + 4 * (l + c), rowb, l0, kapc);
+                const HardXZ b0 = vn_update_fixed<W, ADD, NP>(msg + 4 * (c + T), rowb, l0, kapc);
+                const HardXZ b1 = vn_update_fixed<W, ADD, NP>(msg + 4 * (l + c + T), rowb, l0, kapc);
+                const uint32_t xl = __ballot_sync(0xffffffffu, a0.x), zl = __ballot_sync(0xffffffffu, a0.z);
+                const uint32_t xr = __ballot_sync(0xffffffffu, a1.x), zr = __ballot_sync(0xffffffffu, a1.z);
+                const uint32_t xl2 = __ballot_sync(0xffffffffu, b0.x), zl2 = __ballot_sync(0xffffffffu, b0.z);
+                const uint32_t xr2 = __ballot_sync(0xffffffffu, b1.x), zr2 = __ballot_sync(0xffffffffu, b1.z);
                 if ((tid & 31) == 0) {
                     const int wd = c0 >> 5, wd2 = (c0 + T) >> 5;
                     gm.bits[kXL * nw1 + wd] = xl; gm.bits[kZL * nw1 + wd] = zl;
@@ -980,14 +1042,13 @@ __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, i
 #pragma unroll 1
         for (; c0 < l; c0 += T) {
             const int c = c0 + (tid & 31);
-            uint32_t e2[2] = {0u, 0u};
+            HardXZ eL{false, false}, eR{false, false};
             if (c < l) {
-                e2[0] = vn_update_fixed<W, ADD, NP>(msg + 4 * c, rowb, l0, kapc);
-                e2[1] = vn_update_fixed<W, ADD, NP>(msg + 4 * (l + c), rowb, l0, kapc);
+                eL = vn_update_fixed<W, ADD, NP>(msg + 4 * c, rowb, l0, kapc);
+                eR = vn_update_fixed<W, ADD, NP>(msg + 4 * (l + c), rowb, l0, kapc);
             }
-            const uint32_t eL = e2[0], eR = e2[1];
-            const uint32_t xl = __ballot_sync(0xffffffffu, eL & 1u), zl = __ballot_sync(0xffffffffu, eL >> 1);
-            const uint32_t xr = __ballot_sync(0xffffffffu, eR & 1u), zr = __ballot_sync(0xffffffffu, eR >> 1);
+            const uint32_t xl = __ballot_sync(0xffffffffu, eL.x), zl = __ballot_sync(0xffffffffu, eL.z);
+            const uint32_t xr = __ballot_sync(0xffffffffu, eR.x), zr = __ballot_sync(0xffffffffu, eR.z);
             if ((tid & 31) == 0) {
                 const int wd = c0 >> 5;
                 gm.bits[kXL * nw1 + wd] = xl; gm.bits[kZL * nw1 + wd] = zl;

@@ -103,6 +103,30 @@ __device__ __forceinline__ F2 log1p_01_poly2(F2 t)
     return fma2(p, t, bc(1.0f));
 }
 __device__ __forceinline__ F2 log1p_01_2(F2 t) { return mul2(t, log1p_01_poly2(t)); }
+// -P(t): every coefficient negated.  Rounding to nearest is symmetric in the
+// sign, so each step is exactly the negative of log1p_01_poly2's, and
+// fma(t, -P, L) == fma(-t, P, L) bit for bit -- without the negation op.
+__device__ __forceinline__ F2 log1p_01_npoly2(F2 t)
+{
+    F2 p = fma2(bc(0.003227271f), t, bc(-0.019791102f));
+    p = fma2(p, t, bc(0.05688295f));
+    p = fma2(p, t, bc(-0.106008776f));
+    p = fma2(p, t, bc(0.15308061f));
+    p = fma2(p, t, bc(-0.19678909f));
+    p = fma2(p, t, bc(0.24955378f));
+    p = fma2(p, t, bc(-0.33330205f));
+    p = fma2(p, t, bc(0.49999923f));
+    return fma2(p, t, bc(-1.0f));
+}
+// y >= 0 ? a : b as FSETP + FSEL (the compiler otherwise builds the selected
+// pair with predicated moves, three to four per pair).
+__device__ __forceinline__ float sel_ge0(float y, float a, float b)
+{
+    float d;
+    asm("{\n\t.reg .pred p;\n\tsetp.ge.f32 p, %1, 0f00000000;\n\tselp.f32 %0, %2, %3, p;\n\t}"
+        : "=f"(d) : "f"(y), "f"(a), "f"(b));
+    return d;
+}
 
 // (a & 0x7fffff) | 0x3f800000 as ONE LOP3: with both masks as immediates
 // ptxas splits it in two; the OR constant is kept in a register instead.
@@ -129,8 +153,8 @@ __device__ __forceinline__ F2 vn_F2(float y0, float y1, F2 kapc2)
     const F2 x = pk(-fminf(fabsf(y0), 87.0f), -fminf(fabsf(y1), 87.0f));
     const F2 q = exp_neg2(x);
     const F2 af = fma2(kapc2, q, bc(1.0f)), aa = add2(kapc2, q);
-    const F2 A = pk(y0 >= 0.0f ? lo(af) : lo(aa), y1 >= 0.0f ? hi(af) : hi(aa));
-    return fma2(sub2(bc(0.0f), q), log1p_01_poly2(q), log_pos2(A));
+    const F2 A = pk(sel_ge0(y0, lo(af), lo(aa)), sel_ge0(y1, hi(af), hi(aa)));
+    return fma2(q, log1p_01_npoly2(q), log_pos2(A));  // log(A) - q P(q), one rounding
 }
 
 // rcp_rn on both halves: two MUFU.RCP seeds, the Newton step on FFMA2.

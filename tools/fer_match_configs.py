@@ -6,7 +6,8 @@ reference for the min-sum family -- tests/test_oracle_pins.py).
     python tools/fer_match_configs.py ref [--only ...]        # here: fp64 oracle, cached per point
     python tools/fer_match_configs.py compare --out profiles/fer_match_configs345_r02.json
 
-Points (BASELINE.json configs[2..4], seed 0, matched eps0, marginal VN):
+Points (BASELINE.json configs[2..4], seed 0, matched eps0, marginal VN; `--only c2`
+adds configs[1], the 35-point [[254,28]] sweep, at its own 2^20 frames per point):
   C3  random GB l in {63,127,255,511}, w=5; SAGMS(0.30,0.50,1.10), SMS 0.75; p=0.05; l_max 64
   C4  random GB l=127, w in {3,4,5,6,8}; SMS {0.5,0.75,1.0}, SAGMS, BP4; p=0.04; l_max 100
   C5  [[254,28]] and random GB l=511 w=5; SAGMS; p in {0.03,0.08}; l_max 100
@@ -54,6 +55,10 @@ def code_name(code):
 def points(only=("c3", "c4", "c5")):
     """(config, code, decoder, p, l_max, gpu_frames, ref_frames)."""
     out = []
+    if "c2" in only:  # BASELINE configs[1] at its own size; cheapest points first
+        for p in (0.02, 0.04, 0.06, 0.08, 0.10):
+            for name in ("sagms", "sms0.5", "sms0.625", "sms0.75", "sms0.875", "sms1.0", "bp4"):
+                out.append(("c2", "gb254", name, p, 100, 1 << 20, 1 << 20))
     if "c3" in only:
         for ell in (63, 127, 255, 511):
             for name in ("sagms", "sms0.75"):
