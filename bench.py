@@ -341,6 +341,7 @@ def run_ours(args, rank, world, local_rank):
     c5 = strong_config5(args, rank, world, dev, l2)
     if rank != 0:
         return
+    fer_check = fer_criterion(P, dg, points, dev)
     # ---- roofline of the dominant kernel (min-sum marginal, bicycle W=5) ----
     mins = [k for k, (name, _, _) in enumerate(points) if name != "bp4"]
     ms_mins = sum(launch_ms[k][0] for k in mins) / args.steps
@@ -442,11 +443,50 @@ def run_ours(args, rank, world, local_rank):
         "fer": fer,
     }
     line["strong_config5"] = c5
+    if fer_check:
+        line["fer_check"] = fer_check
     if cpu:
         line["cpu_baseline"] = cpu
     if parity:
         line["parity"] = parity
     print(json.dumps(line), flush=True)
+
+
+def fer_criterion(P, dg, points, dev):
+    """north_star's FER criterion inside the bench run (untimed): every
+    configs[1] point decoded on the frames [0, F) of the committed float64
+    reference counts (tests/golden/fer64_config2.json: the reference's fp64
+    arithmetic on the same Philox frames, F = 2^20 where available); the GPU
+    FER must lie inside the reference's 95% Wilson interval
+    (harness.py:102-125)."""
+    import torch
+    path = os.path.join(ROOT, "tests", "golden", "fer64_config2.json")
+    if not os.path.exists(path) or FRAMES_PER_POINT != 1 << 20:
+        return None
+    with open(path) as fh:
+        ref = json.load(fh)["points"]
+    cnt = torch.zeros((len(points), 4), dtype=torch.int64, device=dev)
+    for k, (name, cfg, p) in enumerate(points):
+        P.decode_frames_device(dg, cfg, p, p, SEED, 0, ref[f"{name}@{p}"]["frames"], counters=cnt[k],
+                               want_frames=False)
+    c = cnt.cpu().numpy()
+    inside, rows, worst = 0, 0, None
+    for k, (name, cfg, p) in enumerate(points):
+        r = ref[f"{name}@{p}"]
+        n, fg, fo = int(c[k, 0]), int(c[k, 1]), r["ref64_failures"]
+        assert n == r["frames"]
+        lo, hi = P.wilson_interval(fo, n)
+        ok = lo <= fg / n <= hi
+        inside += int(ok)
+        rows += 1
+        # distance from the reference FER in units of the interval's half-width
+        d = abs(fg - fo) / max(1e-300, n * (hi - lo) / 2)
+        if worst is None or d > worst["half_widths"]:
+            worst = {"point": f"{name}@{p}", "frames": n, "gpu_failures": fg, "ref64_failures": fo,
+                     "ref64_wilson95": [lo, hi], "half_widths": round(d, 3)}
+    return {"points": rows, "inside_ref64_wilson95": inside, "all_inside": inside == rows,
+            "frames_per_point": sorted({v["frames"] for v in ref.values()}), "worst": worst,
+            "reference": "tests/golden/fer64_config2.json: the reference's float64 arithmetic on the same frames"}
 
 
 def strong_config5(args, rank, world, dev, l2):
