@@ -54,9 +54,10 @@ METRIC = "decoded frames/s and CN-edge updates/s per GPU & 8×B200 (% roofline),
 OPS_PER_EDGE = {"sagms": 30.3 + 4, "sms": 30.0 + 4, "ms": 29.0 + 4, "bp4": 34.1 + 10}
 # FP32-pipe lane operations per BP4 CN-edge update of the fp32 recipe
 # (check side 36.6: exponential 11, prefix/suffix 3.6, merge 4, reciprocal 3
-# (its MUFU seed runs on the XU pipe), ratio 1, logarithm 14; qubit side 10.8
-# per edge); DESIGN.md section 5
-BP4_FP32_OPS = 47.4
+# (its MUFU seed runs on the XU pipe), ratio 1, logarithm 14; qubit side 10.0
+# per edge: 14 sum / belief adds, 2 x 37 for the factor pair, 2 + 10 output
+# adds per 10 edges); DESIGN.md section 5
+BP4_FP32_OPS = 46.6
 
 
 # BASELINE configs[4] (strong scaling): GbSpec args, p values, total frames per point
@@ -383,7 +384,7 @@ def run_ours(args, rank, world, local_rank):
                               "frac": bp4_rate * BP4_FP32_OPS / peak,
                               "ncu_fma_pipe_cycles_active": bp4_hw.get("fma_pipe_cycles_active"),
                               "ncu_issue_slots_busy": bp4_hw.get("issue_slots_busy")},
-                "kernel": "qsg::decode_kernel<5,32,true,false,256> (BP4, marginal VN)",
+                "kernel": "qsg::decode_kernel<5,32,true,false,256,lean> (BP4, marginal VN)",
                 "share_of_step": ms_bp4 / (sum(l[0] for l in launch_ms) / args.steps)}
 
     # ---- CPU baseline on a bounded sample + per-frame parity on that sample ----
@@ -419,7 +420,7 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": len(points) * args.steps,
         "roofline": {"bound": "issue", "achieved": achieved / 1e9, "peak": peak / 1e9, "unit": "Gop/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "qsg::decode_kernel<5,32,false,false,256> (min-sum family, marginal VN, n_pad 256)",
+                     "kernel": "qsg::decode_kernel<5,32,false,false,256,lean> (min-sum family, marginal VN, n_pad 256)",
                      "ops_per_cn_edge_update": "SURVEY.md 8(d): SAGMS 34.3, SMS 34.0",
                      "peak_basis": "148 SMs x 128 lane-instr/clk x measured median SM clock",
                      "share_of_step": share,

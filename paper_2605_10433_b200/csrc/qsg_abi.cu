@@ -361,14 +361,14 @@ int raise_smem_limit(void *fn, int device, int max_smem)
 }
 
 // Pick groups-per-CTA maximising resident frames per SM for one kernel.
-int launch_cfg(qsg_graph *g, bool bp4, bool add, void *fn, qsg::LaunchCfg *out)
+int launch_cfg(qsg_graph *g, bool bp4, bool add, bool lean, void *fn, qsg::LaunchCfg *out)
 {
     int max_smem = 0;
     QSG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
     int rc = raise_smem_limit(fn, g->device, max_smem);
     if (rc) return rc;
     std::lock_guard<std::mutex> lock(g->mu);
-    qsg::LaunchCfg &c = g->cfg_cache[bp4][add];
+    qsg::LaunchCfg &c = g->cfg_cache[bp4][add][lean];
     if (c.ok) { *out = c; return QSG_OK; }
     const int T = g->threads;
     cudaFuncAttributes fa;
@@ -399,15 +399,30 @@ int launch_cfg(qsg_graph *g, bool bp4, bool add, void *fn, qsg::LaunchCfg *out)
     return QSG_OK;
 }
 
+// (threads, n_pad) pairs with a compile-time qubit stride: the shapes that
+// have a lean instance (qsg_inst.cuh)
+bool lean_kernel_exists(const qsg_graph *g)
+{
+    if (g->kind <= 0) return false;
+    const int T = g->threads, np = g->n_pad;
+    return (T == 32 && (np == 256 || np == 128)) || (T == 64 && np == 512) || (T == 128 && (np == 512 || np == 1024));
+}
+
 int launch_decode(qsg_graph *g, const qsg_decoder_cfg *cfg, qsg::KParams &p, cudaStream_t st)
 {
     const bool bp4 = cfg->variant == QSG_BP4, add = cfg->vn_mode == QSG_VN_ADDITIVE;
     if (!bp4 && g->d_cn_tab_x) p.cn_tab = g->d_cn_tab_x;
+    // the lean instance (qsg_kernel.cuh) serves the production shape: no
+    // traces, no e_hat, early stop, closed-form first iteration, 4 lanes per
+    // syndrome word, gains from the table; QSG_NO_LEAN=1 disables it (tests)
+    static const bool no_lean = std::getenv("QSG_NO_LEAN") != nullptr;
+    const bool lean = !no_lean && lean_kernel_exists(g) && !add && p.first_fast && p.early_stop && !p.out_ehat &&
+                      !p.tr_unsat && !p.tr_vn && !p.tr_cn && !p.tr_counts && g->lpw == 4 && p.m < qsg::kGainTab;
     void *fn = qsg::kernel_ptr(g->kind, g->threads, bp4, add,
-                               g->kind > 0 ? g->n_pad : std::max(g->dc_max, g->dv_max));
+                               g->kind > 0 ? g->n_pad : std::max(g->dc_max, g->dv_max), lean);
     if (!fn) return fail(QSG_EUNSUPPORTED, "no kernel for this graph kind");
     qsg::LaunchCfg lc;
-    int rc = launch_cfg(g, bp4, add, fn, &lc);
+    int rc = launch_cfg(g, bp4, add, lean, fn, &lc);
     if (rc) return rc;
     if (p.count == 0) return QSG_OK;
     const int64_t want = (p.count + lc.groups - 1) / lc.groups;
@@ -475,6 +490,11 @@ void fill_cfg_params(const qsg_decoder_cfg *c, double l0, qsg::KParams &p)
     // recipe evaluated here once instead of a double division per iteration
     // and frame; volatile keeps each product rounded (no contraction)
     p.use_gtab = (p.gain_mode == 2 && p.m < qsg::kGainTab) ? 1 : 0;
+    if (p.gain_mode != 2 && p.m < qsg::kGainTab) {
+        // lean kernels read the gains of every variant from the table
+        const float gc = p.gain_mode == 1 ? p.alpha : 1.0f;
+        for (int u = 0; u <= p.m; ++u) p.gtab[2 * u] = p.gtab[2 * u + 1] = gc;
+    }
     if (p.use_gtab) {
         for (int u = 0; u <= p.m; ++u) {
             const double gamma = (double)u / (double)p.m;
@@ -589,16 +609,16 @@ int create_common(int32_t device, qsg_graph **out, qsg_graph **g)
 }  // namespace
 
 namespace qsg {
-void *kernel_ptr(int W, int T, bool bp4, bool additive, int np)
+void *kernel_ptr(int W, int T, bool bp4, bool additive, int np, bool lean)
 {
     switch (W) {
-    case 0: return kernel_ptr_w0(T, bp4, additive, np);
-    case 2: return kernel_ptr_w2(T, bp4, additive, np);
-    case 3: return kernel_ptr_w3(T, bp4, additive, np);
-    case 4: return kernel_ptr_w4(T, bp4, additive, np);
-    case 5: return kernel_ptr_w5(T, bp4, additive, np);
-    case 6: return kernel_ptr_w6(T, bp4, additive, np);
-    case 8: return kernel_ptr_w8(T, bp4, additive, np);
+    case 0: return kernel_ptr_w0(T, bp4, additive, np, lean);
+    case 2: return kernel_ptr_w2(T, bp4, additive, np, lean);
+    case 3: return kernel_ptr_w3(T, bp4, additive, np, lean);
+    case 4: return kernel_ptr_w4(T, bp4, additive, np, lean);
+    case 5: return kernel_ptr_w5(T, bp4, additive, np, lean);
+    case 6: return kernel_ptr_w6(T, bp4, additive, np, lean);
+    case 8: return kernel_ptr_w8(T, bp4, additive, np, lean);
     default: return nullptr;
     }
 }

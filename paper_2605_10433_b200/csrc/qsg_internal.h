@@ -19,14 +19,14 @@ constexpr int kBicycleWs[] = {2, 3, 4, 5, 6, 8};
 constexpr int kThreadCounts[] = {32, 128};
 
 // Returns the __global__ function for (W, T, bp4, additive) or nullptr.
-void *kernel_ptr(int W, int T, bool bp4, bool additive, int np);
-void *kernel_ptr_w0(int T, bool bp4, bool additive, int np);
-void *kernel_ptr_w2(int T, bool bp4, bool additive, int np);
-void *kernel_ptr_w3(int T, bool bp4, bool additive, int np);
-void *kernel_ptr_w4(int T, bool bp4, bool additive, int np);
-void *kernel_ptr_w5(int T, bool bp4, bool additive, int np);
-void *kernel_ptr_w6(int T, bool bp4, bool additive, int np);
-void *kernel_ptr_w8(int T, bool bp4, bool additive, int np);
+void *kernel_ptr(int W, int T, bool bp4, bool additive, int np, bool lean);
+void *kernel_ptr_w0(int T, bool bp4, bool additive, int np, bool lean);
+void *kernel_ptr_w2(int T, bool bp4, bool additive, int np, bool lean);
+void *kernel_ptr_w3(int T, bool bp4, bool additive, int np, bool lean);
+void *kernel_ptr_w4(int T, bool bp4, bool additive, int np, bool lean);
+void *kernel_ptr_w5(int T, bool bp4, bool additive, int np, bool lean);
+void *kernel_ptr_w6(int T, bool bp4, bool additive, int np, bool lean);
+void *kernel_ptr_w8(int T, bool bp4, bool additive, int np, bool lean);
 
 struct LaunchCfg {
     int groups = 0;        // groups (frames in flight) per CTA
@@ -60,7 +60,7 @@ struct qsg_graph {
     uint32_t tab_bytes = 0, group_bytes = 0;
     // launch configurations cached per kernel instance
     std::mutex mu;
-    qsg::LaunchCfg cfg_cache[2][2];  // [bp4][additive]
+    qsg::LaunchCfg cfg_cache[2][2][2];  // [bp4][additive][lean]
     // frame-queue counter per stream: launches on one stream are ordered, so
     // one 8-byte counter (re-zeroed before each launch) serves them all; no
     // per-launch allocation (the stream-ordered pool returns freed memory at

@@ -508,7 +508,11 @@ __device__ __forceinline__ SynPlan<W> syn_plan(const KParams &p, const GroupMem 
     return P;
 }
 
-template <int W, int T>
+// BASE: out[w] = base[w] ^ parity (the residual against the observed
+// syndrome); else out[w] = parity (a compile-time flag: a run-time null test
+// of a shared-memory pointer costs eight instructions of generic-address
+// arithmetic per iteration).
+template <int W, int T, bool BASE>
 __device__ __forceinline__ int circ_syndrome_plan(const SynPlan<W> &P, const GroupMem &gm, const uint32_t *base,
                                                   uint32_t *out, int lpw)
 {
@@ -527,7 +531,9 @@ __device__ __forceinline__ int circ_syndrome_plan(const SynPlan<W> &P, const Gro
         if (o < lpw) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
     int cnt = 0;
     if (P.writer) {
-        const uint32_t v = ((base ? base[P.w] : 0u) ^ acc) & P.mask;
+        uint32_t v = acc;
+        if constexpr (BASE) v ^= base[P.w];
+        v &= P.mask;
         out[P.w] = v;
         cnt = __popc(v);
     }
@@ -1165,9 +1171,21 @@ constexpr int max_threads(int W, bool BP4, int NP)
     return W == 8 ? 384 : (W == 6 ? 512 : (BP4 ? QSG_BP4_THREADS : 640));
 }
 
-template <int W, int T, bool BP4, bool ADD, int NP>
+// LEAN: the production shape of a bicycle launch, compiled without the
+// run-time options the iteration loop otherwise tests every iteration --
+// no traces / snapshots, no e_hat output, early stop on, the windowed
+// syndrome plan with 4 lanes per word (every bicycle shape the host builds
+// with about four circulant indices per thread), the closed-form first
+// iteration (v0 > 0) and gains for every variant from KParams::gtab (the
+// host fills it with 1 / alpha / the SAGMS recipe).  The host selects it
+// when all of that holds (launch_decode); the serial
+// syndrome -> reduce -> exit-test -> gains section between the qubit and
+// check phases is ~40% shorter.  Results are identical by construction:
+// the same phases run, only the option tests are folded.
+template <int W, int T, bool BP4, bool ADD, int NP, bool LEAN = false>
 __global__ void __launch_bounds__(max_threads(W, BP4, NP), W == 0 ? 1 : 0) decode_kernel(const KParams p)
 {
+    static_assert(!LEAN || (W > 0 && !ADD), "lean kernels: bicycle, marginal");
     extern __shared__ __align__(16) unsigned char smem[];
     // ---- per-CTA copy of the graph tables ----
     const uint32_t tabw = (uint32_t)p.m_pad * p.row_words;
@@ -1213,12 +1231,13 @@ __global__ void __launch_bounds__(max_threads(W, BP4, NP), W == 0 ? 1 : 0) decod
     // hard decision with all-zero check messages: argmin(0, L0, L0, L0)
     const uint32_t hd0 = hard_decision(p.l0, p.l0, p.l0);
     // bicycle residual plan (loop-invariant syndrome windows), lpw >= 4
-    const bool use_plan = W > 0 && p.lpw >= 4;
+    const bool use_plan = LEAN || (W > 0 && p.lpw >= 4);
+    const int lpw = LEAN ? 4 : p.lpw;
     SynPlan<(W > 0 ? W : 1)> plan;
     if constexpr (W > 0) {
         if (use_plan) plan = syn_plan<W, T>(p, gm, tid);
     }
-    const bool capture = p.tr_vn != nullptr || p.tr_cn != nullptr;
+    const bool capture = !LEAN && (p.tr_vn != nullptr || p.tr_cn != nullptr);
 
     // frame queue: the index of the NEXT frame is fetched as soon as the
     // current one is known, so the global atomic's round trip overlaps the
@@ -1257,7 +1276,7 @@ __global__ void __launch_bounds__(max_threads(W, BP4, NP), W == 0 ? 1 : 0) decod
                 group_sync<T>(g);
                 bitmaps_from_bytes<T>(p, gm, eb, tid);
                 group_sync<T>(g);
-                if (use_plan) circ_syndrome_plan<W, T>(plan, gm, nullptr, gm.synw, p.lpw);
+                if (use_plan) circ_syndrome_plan<W, T, false>(plan, gm, nullptr, gm.synw, lpw);
                 else circ_syndrome<W, T>(p, gm, nullptr, gm.synw, tid);
                 group_sync<T>(g);  // every warp done reading the bitmaps before they are reset below
             } else if (p.syn_words) {
@@ -1320,7 +1339,7 @@ __global__ void __launch_bounds__(max_threads(W, BP4, NP), W == 0 ? 1 : 0) decod
         }
         // the initial qubit->check messages (v0); not needed when the first
         // check update is the closed form, which writes every edge slot
-        if (!(W > 0 && p.first_fast)) {
+        if (!LEAN && !(W > 0 && p.first_fast)) {
             const uint32_t v0b = f2u(p.v0);
             for (int s = tid; s < msg_words; s += T) sts_u(gm.msg, 4u * s, v0b);
         }
@@ -1331,7 +1350,7 @@ __global__ void __launch_bounds__(max_threads(W, BP4, NP), W == 0 ? 1 : 0) decod
             uint32_t res = 0;
             int part;
             if constexpr (W > 0) {
-                part = use_plan ? circ_syndrome_plan<W, T>(plan, gm, gm.synw, gm.resw, p.lpw)
+                part = use_plan ? circ_syndrome_plan<W, T, true>(plan, gm, gm.synw, gm.resw, lpw)
                                 : circ_syndrome<W, T>(p, gm, gm.synw, gm.resw, tid);
             } else {
                 res = syn_bits ^ syndrome_bits_generic<T, (NP > 0 ? NP : kGenericMaxDeg)>(p, gm, tid);
@@ -1339,43 +1358,50 @@ __global__ void __launch_bounds__(max_threads(W, BP4, NP), W == 0 ? 1 : 0) decod
             }
             const int unsat = group_sum<T>(part, scratch, ell & 1, tid, g);
             if constexpr (W > 0 && T == 32) __syncwarp();  // resw visible to the check phase
-            if (p.tr_unsat && tid == 0) p.tr_unsat[f * p.l_max + n_gamma] = unsat;
-            ++n_gamma;
-            if (unsat == 0 && !recorded) {
-                success = 1;
-                iters = ell;
-                recorded = 1;
-                if (p.out_ehat)
-                    for (int j = tid; j < n; j += T) p.out_ehat[f * n + j] = ehat_of<W>(p, gm, j);
-            }
-            if (p.early_stop && unsat == 0) break;
-            if (ell == p.l_max) {
-                if (!recorded && p.out_ehat)
-                    for (int j = tid; j < n; j += T) p.out_ehat[f * n + j] = ehat_of<W>(p, gm, j);
-                if (!capture) break;
-            }
             float g0 = 1.0f, g1 = 1.0f;
-            if (p.gain_mode == 1) {
-                g0 = g1 = p.alpha;
-            } else if (p.gain_mode == 2) {
-                if (p.use_gtab) {  // the same double recipe, tabulated per unsat count by the host
-                    g0 = p.gtab[2 * unsat];
-                    g1 = p.gtab[2 * unsat + 1];
-                } else {
-                    const double gamma = (double)unsat / (double)m;
-                    const double base = p.amax - (p.amax - p.amin) * gamma;
-                    g0 = (float)(base * 1.0);
-                    g1 = (float)(base * p.eta);
+            if constexpr (LEAN) {
+                if (unsat == 0) { success = 1; iters = ell; break; }
+                if (ell == p.l_max) break;
+                g0 = p.gtab[2 * unsat];
+                g1 = p.gtab[2 * unsat + 1];
+            } else {
+                if (p.tr_unsat && tid == 0) p.tr_unsat[f * p.l_max + n_gamma] = unsat;
+                ++n_gamma;
+                if (unsat == 0 && !recorded) {
+                    success = 1;
+                    iters = ell;
+                    recorded = 1;
+                    if (p.out_ehat)
+                        for (int j = tid; j < n; j += T) p.out_ehat[f * n + j] = ehat_of<W>(p, gm, j);
+                }
+                if (p.early_stop && unsat == 0) break;
+                if (ell == p.l_max) {
+                    if (!recorded && p.out_ehat)
+                        for (int j = tid; j < n; j += T) p.out_ehat[f * n + j] = ehat_of<W>(p, gm, j);
+                    if (!capture) break;
+                }
+                if (p.gain_mode == 1) {
+                    g0 = g1 = p.alpha;
+                } else if (p.gain_mode == 2) {
+                    if (p.use_gtab) {  // the same double recipe, tabulated per unsat count by the host
+                        g0 = p.gtab[2 * unsat];
+                        g1 = p.gtab[2 * unsat + 1];
+                    } else {
+                        const double gamma = (double)unsat / (double)m;
+                        const double base = p.amax - (p.amax - p.amin) * gamma;
+                        g0 = (float)(base * 1.0);
+                        g1 = (float)(base * p.eta);
+                    }
                 }
             }
-            if (W > 0 && ell == 1 && p.first_fast)
+            if (W > 0 && ell == 1 && (LEAN || p.first_fast))
                 cn_phase_first<(W > 0 ? W : 1), T, BP4>(p, gm, g0, g1, tid);
             else
                 cn_phase<W, T, BP4, NP>(p, gm, syn_bits, res, g0, g1, tid);
             group_sync<T>(g);
             if (capture && p.tr_cn) snapshot<T>(p, gm.msg, p.tr_cn + (f * p.l_max + n_snap) * p.E, tid, false);
             if constexpr (W > 0 && W <= 5 && !BP4 && !ADD) {
-                if (ell == 1 && p.first_fast)
+                if (ell == 1 && (LEAN || p.first_fast))
                     vn_phase_first<(W > 0 ? W : 1), T, NP>(p, gm, g0, g1, tid);
                 else
                     vn_phase<W, T, BP4, ADD, NP>(p, gm, tid);
@@ -1391,7 +1417,7 @@ __global__ void __launch_bounds__(max_threads(W, BP4, NP), W == 0 ? 1 : 0) decod
         if (tid == 0) {
             if (p.out_flag) p.out_flag[f] = (uint8_t)(p.sample ? !success : success);
             if (p.out_iters) p.out_iters[f] = iters;
-            if (p.tr_counts) { p.tr_counts[2 * f] = n_gamma; p.tr_counts[2 * f + 1] = n_snap; }
+            if (!LEAN && p.tr_counts) { p.tr_counts[2 * f] = n_gamma; p.tr_counts[2 * f + 1] = n_snap; }
             tally[0] += 1ull;
             tally[1] += (unsigned long long)!success;
             tally[2] += (unsigned long long)iters;

@@ -55,8 +55,13 @@ def test_kernels_are_sm100a():
         elif cur:
             funcs[cur].append(ln)
     # the BASELINE configs[1] kernels (W = 5, one warp per frame, n_pad 256)
-    ms = "\n".join(funcs["_ZN3qsg13decode_kernelILi5ELi32ELb0ELb0ELi256EEEvNS_7KParamsE"])
-    bp4 = "\n".join(funcs["_ZN3qsg13decode_kernelILi5ELi32ELb1ELb0ELi256EEEvNS_7KParamsE"])
+    # (lean instances, the ones the bench launches: template flag LEAN = true)
+    ms = "\n".join(funcs["_ZN3qsg13decode_kernelILi5ELi32ELb0ELb0ELi256ELb1EEEvNS_7KParamsE"])
+    bp4 = "\n".join(funcs["_ZN3qsg13decode_kernelILi5ELi32ELb1ELb0ELi256ELb1EEEvNS_7KParamsE"])
+    full = [funcs["_ZN3qsg13decode_kernelILi5ELi32ELb0ELb0ELi256ELb0EEEvNS_7KParamsE"],
+            funcs["_ZN3qsg13decode_kernelILi5ELi32ELb1ELb0ELi256ELb0EEEvNS_7KParamsE"]]
+    # the lean instances fold the run-time options: markedly less code
+    assert len(ms.splitlines()) < 0.8 * len(full[0]) and len(bp4.splitlines()) < 0.8 * len(full[1])
     # min-sum: min1/min2 with the sign product riding on min (FMNMX), paired
     # qubit factors (FFMA2), frame queue (ATOMG), ballot-packed bitmaps (VOTE)
     for op in ("FMNMX", "FFMA2", "ATOMG", "VOTE", "LDS.U16", "SHFL"):
@@ -67,7 +72,7 @@ def test_kernels_are_sm100a():
     # double divisions outside the recipes), and neither spills
     for op in ("FFMA2", "FMUL2"):
         assert op in bp4, op
-    for k in (ms, bp4):
+    for k in (ms, bp4, "\n".join(full[0]), "\n".join(full[1])):
         assert "MUFU.EX2" not in k and "MUFU.LG2" not in k
         assert "STL" not in k and "LDL" not in k
 

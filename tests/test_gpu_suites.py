@@ -243,3 +243,28 @@ def test_concurrent_host_threads_on_one_stream(P):
     for t in ts:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("spec", [GB254, (63, (0, 3, 11, 20, 44), (0, 7, 19, 33, 52)),
+                                  (255, (0, 9, 77, 130, 201), (0, 40, 101, 166, 240)),
+                                  (511, (0, 5, 200, 397, 418), (0, 81, 284, 347, 418)),
+                                  (127, (0, 15, 66), (0, 58, 121))])
+@pytest.mark.parametrize("variant,kw", [("sagms", dict(gain=(0.30, 0.50, 1.10))), ("sms", dict(alpha=0.75)),
+                                        ("ms", {}), ("bp4", {})])
+def test_lean_and_full_instances_agree(P, oracle, spec, variant, kw):
+    """A launch without traces / e_hat runs the lean kernel instance (its
+    run-time options folded at compile time), one asking for e_hat the full
+    instance: same frames, same outcomes, and both equal to the oracle."""
+    g = P.gb_graph(P.GbSpec(*spec))
+    if "gain" in kw:
+        kw = dict(gain=P.GainParams(*kw["gain"]))
+    cfg = P.DecoderConfig(variant, l_max=40, **kw)
+    n = 700
+    cnt = torch.zeros(4, dtype=torch.int64, device="cuda")
+    f1, i1, _ = P.decode_frames_device(g, cfg, 0.07, 0.07, 5, 11, n, counters=cnt)
+    f2, i2, e2 = P.decode_frames_device(g, cfg, 0.07, 0.07, 5, 11, n, want_ehat=True)
+    assert torch.equal(f1, f2) and torch.equal(i1, i2)
+    of, oi, oe, oc = oracle.frames(g, cfg, 0.07, 0.07, 5, 11, n, want_ehat=True)
+    assert np.array_equal(f1.cpu().numpy().astype(bool), of) and np.array_equal(i1.cpu().numpy(), oi)
+    assert np.array_equal(e2.cpu().numpy(), oe)
+    assert cnt.cpu().tolist() == [int(x) for x in oc]

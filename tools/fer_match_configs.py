@@ -111,12 +111,15 @@ def gpu(only, out_dir):
         print(key(pt), nf, int(f.sum()), f"{dt:.2f}s", flush=True)
 
 
-def ref(only, threads):
+def ref(only, threads, p_only=None, cache=None):
     from oracle import oracle as O
-    os.makedirs(CACHE, exist_ok=True)
+    cache = cache or CACHE
+    os.makedirs(cache, exist_ok=True)
     for pt in points(only):
         cfg, code, name, p, l_max, _, nr = pt
-        path = os.path.join(CACHE, key(pt) + f"_{nr}.npz")
+        if p_only is not None and p != p_only:
+            continue
+        path = os.path.join(cache, key(pt) + f"_{nr}.npz")
         if os.path.exists(path):
             continue
         ell, a, b = spec_of(code)
@@ -185,12 +188,14 @@ if __name__ == "__main__":
     ap.add_argument("--gpu-dir", default=os.path.join(ROOT, "gpurun_out", "fer_cfg"))
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "fer_match_configs345_r02.json"))
     ap.add_argument("--threads", type=int, default=None)
+    ap.add_argument("--p-only", type=float, default=None, help="ref: only the points at this p")
+    ap.add_argument("--cache-dir", default=None, help="ref: where the fp64 outcomes are cached")
     a = ap.parse_args()
     only = tuple(a.only.split(","))
     if a.mode == "gpu":
         gpu(only, a.gpu_dir)
     elif a.mode == "ref":
-        ref(only, a.threads)
+        ref(only, a.threads, a.p_only, a.cache_dir)
     elif a.mode == "list":
         for pt in points(only):
             print(key(pt), pt[5], pt[6])
