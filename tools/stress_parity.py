@@ -58,6 +58,9 @@ for i in range(cases):
     of, oi, oe, _ = oracle.frames(g, cfg, p, p, seed, start, count, want_ehat=True)
     ok = (np.array_equal(f.cpu().numpy().astype(bool), of) and np.array_equal(it.cpu().numpy(), oi)
           and np.array_equal(eh.cpu().numpy(), oe))
+    # the same frames without e_hat: the lean kernel instance where one exists
+    f2, it2, _ = P.decode_frames_device(g, cfg, p, p, seed, start, count)
+    ok = ok and np.array_equal(f2.cpu().numpy().astype(bool), of) and np.array_equal(it2.cpu().numpy(), oi)
     bad += not ok
     print(f"{'ok ' if ok else 'BAD'} l={ell} w={w} kind={g.kind} T={g.threads} {variant} {cfg.vn_mode} l_max={cfg.l_max} "
           f"p={p:.3f} frames={count}", flush=True)
