@@ -280,12 +280,21 @@ struct GroupMem {
     const int32_t *gbexp;    // bicycle: a exponents [0, 8), b exponents [8, 16)
     unsigned char *msg;      // fp32 messages, slot-major
     uint32_t *ehat;          // generic only: one Pauli code per qubit
-    uint32_t *bits;          // bicycle: XL, ZL, XR, ZR circulant bitmaps, nw+1 words each
+    uint32_t *bits;          // bicycle: XL, ZL, XR, ZR circulant bitmaps, nw+1 words each, word-interleaved (bidx)
     uint32_t *synw;          // bicycle: observed syndrome words (X checks, then Z checks)
     uint32_t *resw;          // bicycle: residual syndrome words
 };
 
 enum { kXL = 0, kZL = 1, kXR = 2, kZR = 3 };
+// Bitmap word wd of block blk lives at gm.bits[4 * wd + blk]: the four words
+// a warp ballots per 32-qubit step are one 16-byte store (the area is
+// 16-byte aligned), and a bitmap is read with a stride of four words.
+__device__ __forceinline__ int bidx(int blk, int wd) { return 4 * wd + blk; }
+__device__ __forceinline__ void store_bits4(uint32_t *bits, int wd, uint32_t xl, uint32_t zl, uint32_t xr,
+                                            uint32_t zr)
+{
+    *reinterpret_cast<uint4 *>(bits + 4 * wd) = make_uint4(xl, zl, xr, zr);
+}
 
 // ---- check-phase helpers ---------------------------------------------------
 // The check phase is bound by the half-rate ALU pipe (FMNMX / FSETP / SEL /
@@ -381,7 +390,7 @@ __device__ __forceinline__ uint32_t syndrome_bits_generic(const KParams &p, cons
 __device__ __forceinline__ uint32_t circ_window(const uint32_t *B, int l, int start)
 {
     const int q = start >> 5;
-    uint32_t w = __funnelshift_r(B[q], B[q + 1], start & 31);
+    uint32_t w = __funnelshift_r(B[4 * q], B[4 * (q + 1)], start & 31);  // words of one bitmap: stride 4
     const int n1 = l - start;
     if (n1 < 32) w |= B[0] << n1;
     return w;
@@ -409,8 +418,8 @@ __device__ __forceinline__ int circ_syndrome(const KParams &p, const GroupMem &g
     if (w < 2 * nw) {
         zc = w >= nw;
         ww = zc ? w - nw : w;
-        const uint32_t *BL = gm.bits + (zc ? kXL : kZL) * (nw + 1);
-        const uint32_t *BR = gm.bits + (zc ? kXR : kZR) * (nw + 1);
+        const uint32_t *BL = gm.bits + (zc ? kXL : kZL);
+        const uint32_t *BR = gm.bits + (zc ? kXR : kZR);
         for (int k = sub; k < 2 * W; k += lpw) {
             const bool left = k < W;
             // X: left a_k, right b_k; Z: left -b_k, right -a_k
@@ -474,7 +483,7 @@ __device__ __forceinline__ SynPlan<W> syn_plan(const KParams &p, const GroupMem 
     const int nw = p.nw, l = p.ell, lpw = p.lpw;
     const int w = tid / lpw, sub = tid - w * lpw;
     const uint32_t bits_s = smem_addr(gm.bits);
-    const uint32_t zero = bits_s + 4u * (uint32_t)nw;  // XL padding word (always 0)
+    const uint32_t zero = bits_s + 16u * (uint32_t)nw;  // XL padding word (always 0)
     P.w = -1; P.mask = 0u; P.writer = false;
 #pragma unroll
     for (int j = 0; j < SynPlan<W>::K; ++j) {
@@ -498,9 +507,9 @@ __device__ __forceinline__ SynPlan<W> syn_plan(const KParams &p, const GroupMem 
                 start = start >= l ? start - l : start;
                 start = start >= l ? start - l : start;
                 const int blk = left ? (zc ? kXL : kZL) : (zc ? kXR : kZR);
-                const uint32_t b0 = bits_s + 4u * (uint32_t)(blk * (nw + 1));
+                const uint32_t b0 = bits_s + 4u * (uint32_t)blk;
                 const uint32_t n1 = (uint32_t)(l - start);
-                P.lo[j] = (b0 + 4u * (uint32_t)(start >> 5)) | ((uint32_t)(start & 31) << 24);
+                P.lo[j] = (b0 + 16u * (uint32_t)(start >> 5)) | ((uint32_t)(start & 31) << 24);
                 P.hi[j] = b0 | ((n1 < 32u ? n1 : 32u) << 24);
             }
         }
@@ -520,7 +529,7 @@ __device__ __forceinline__ int circ_syndrome_plan(const SynPlan<W> &P, const Gro
 #pragma unroll
     for (int j = 0; j < SynPlan<W>::K; ++j) {
         const uint32_t a = P.lo[j] & 0x00ffffffu, b = P.hi[j] & 0x00ffffffu;
-        uint32_t x = __funnelshift_r(lds_u32(a), lds_u32(a + 4u), P.lo[j] >> 24);
+        uint32_t x = __funnelshift_r(lds_u32(a), lds_u32(a + 16u), P.lo[j] >> 24);
         x |= shl_clamp(lds_u32(b), P.hi[j] >> 24);
         acc ^= x;
     }
@@ -545,7 +554,6 @@ template <int T>
 __device__ __forceinline__ void bitmaps_from_bytes(const KParams &p, const GroupMem &gm, const uint8_t *e, int tid)
 {
     const int l = p.ell;
-    const int nw1 = p.nw + 1;
     for (int c0 = tid & ~31; c0 < 32 * p.nw; c0 += T) {
         const int c = c0 + (tid & 31);
         const uint32_t eL = c < l ? e[c] : 0u, eR = c < l ? e[l + c] : 0u;
@@ -553,8 +561,7 @@ __device__ __forceinline__ void bitmaps_from_bytes(const KParams &p, const Group
         const uint32_t xr = __ballot_sync(0xffffffffu, eR & 1u), zr = __ballot_sync(0xffffffffu, eR >> 1);
         if ((tid & 31) == 0) {
             const int wd = c0 >> 5;
-            gm.bits[kXL * nw1 + wd] = xl; gm.bits[kZL * nw1 + wd] = zl;
-            gm.bits[kXR * nw1 + wd] = xr; gm.bits[kZR * nw1 + wd] = zr;
+            store_bits4(gm.bits, wd, xl, zl, xr, zr);
         }
     }
 }
@@ -991,7 +998,7 @@ __device__ __forceinline__ void vn_phase_first(const KParams &p, const GroupMem 
     // the words cn_phase_first stored: +m0 (satisfied), -m1 (unsatisfied)
     const float A = fminf(g0 * a, kClip), nB = -fminf(g1 * a, kClip);
     const FirstTab<W> t = first_tab<W>(A, nB, p.kapc, (uint32_t)tid & 31u);
-    const int l = p.ell, nw1 = p.nw + 1;
+    const int l = p.ell;
     const float l0 = p.l0;
 #pragma unroll 1
     for (int c0 = tid & ~31; c0 < l; c0 += T) {
@@ -1004,8 +1011,7 @@ __device__ __forceinline__ void vn_phase_first(const KParams &p, const GroupMem 
         const uint32_t xr = __ballot_sync(0xffffffffu, ok && eR.x), zr = __ballot_sync(0xffffffffu, ok && eR.z);
         if ((tid & 31) == 0) {
             const int wd = c0 >> 5;
-            gm.bits[kXL * nw1 + wd] = xl; gm.bits[kZL * nw1 + wd] = zl;
-            gm.bits[kXR * nw1 + wd] = xr; gm.bits[kZR * nw1 + wd] = zr;
+            store_bits4(gm.bits, wd, xl, zl, xr, zr);
         }
     }
 }
@@ -1019,7 +1025,7 @@ __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, i
     if constexpr (W > 0) {
         // thread owns qubits c and l + c; the warp ballots their hard
         // decisions into word c >> 5 of the circulant bitmaps
-        const int l = p.ell, nw1 = p.nw + 1;
+        const int l = p.ell;
         int c0 = tid & ~31;
         if constexpr (!BP4 && T > 32) {
             // two circulant indices (four qubits) per step while both are full
@@ -1038,10 +1044,8 @@ __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, i
                 const uint32_t xr2 = __ballot_sync(0xffffffffu, b1.x), zr2 = __ballot_sync(0xffffffffu, b1.z);
                 if ((tid & 31) == 0) {
                     const int wd = c0 >> 5, wd2 = (c0 + T) >> 5;
-                    gm.bits[kXL * nw1 + wd] = xl; gm.bits[kZL * nw1 + wd] = zl;
-                    gm.bits[kXR * nw1 + wd] = xr; gm.bits[kZR * nw1 + wd] = zr;
-                    gm.bits[kXL * nw1 + wd2] = xl2; gm.bits[kZL * nw1 + wd2] = zl2;
-                    gm.bits[kXR * nw1 + wd2] = xr2; gm.bits[kZR * nw1 + wd2] = zr2;
+                    store_bits4(gm.bits, wd, xl, zl, xr, zr);
+                    store_bits4(gm.bits, wd2, xl2, zl2, xr2, zr2);
                 }
             }
         }
@@ -1059,8 +1063,7 @@ __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, i
                 const uint32_t xr = __ballot_sync(0xffffffffu, eR.x), zr = __ballot_sync(0xffffffffu, eR.z);
                 if ((tid & 31) == 0) {
                     const int wd = c0 >> 5;
-                    gm.bits[kXL * nw1 + wd] = xl; gm.bits[kZL * nw1 + wd] = zl;
-                    gm.bits[kXR * nw1 + wd] = xr; gm.bits[kZR * nw1 + wd] = zr;
+                    store_bits4(gm.bits, wd, xl, zl, xr, zr);
                 }
             }
         }
@@ -1076,8 +1079,7 @@ __device__ __forceinline__ void vn_phase(const KParams &p, const GroupMem &gm, i
             const uint32_t xr = __ballot_sync(0xffffffffu, eR.x), zr = __ballot_sync(0xffffffffu, eR.z);
             if ((tid & 31) == 0) {
                 const int wd = c0 >> 5;
-                gm.bits[kXL * nw1 + wd] = xl; gm.bits[kZL * nw1 + wd] = zl;
-                gm.bits[kXR * nw1 + wd] = xr; gm.bits[kZR * nw1 + wd] = zr;
+                store_bits4(gm.bits, wd, xl, zl, xr, zr);
             }
         }
     } else {
@@ -1157,11 +1159,10 @@ template <int W>
 __device__ __forceinline__ uint8_t ehat_of(const KParams &p, const GroupMem &gm, int j)
 {
     if constexpr (W > 0) {
-        const int nw1 = p.nw + 1;
         const bool right = j >= p.ell;
         const int c = right ? j - p.ell : j;
-        const uint32_t x = gm.bits[(right ? kXR : kXL) * nw1 + (c >> 5)] >> (c & 31);
-        const uint32_t z = gm.bits[(right ? kZR : kZL) * nw1 + (c >> 5)] >> (c & 31);
+        const uint32_t x = gm.bits[bidx(right ? kXR : kXL, c >> 5)] >> (c & 31);
+        const uint32_t z = gm.bits[bidx(right ? kZR : kZL, c >> 5)] >> (c & 31);
         return (uint8_t)((x & 1u) | ((z & 1u) << 1));
     } else {
         return (uint8_t)gm.ehat[j];
@@ -1291,7 +1292,7 @@ __global__ void __launch_bounds__(max_threads(W, BP4, NP), W == 0 ? 1 : 0) decod
                     for (int q = 0; q < 4; ++q)
                         if (4 * b + q < n) eb[4 * b + q] = pauli_from_word(w.v[q], p.kx, p.ky, p.kz);
                 }
-                if (tid < 4) gm.bits[tid * (p.nw + 1) + p.nw] = 0u;  // padding words (the rest is written below)
+                if (tid < 4) gm.bits[bidx(tid, p.nw)] = 0u;  // padding words (the rest is written below)
                 group_sync<T>(g);
                 bitmaps_from_bytes<T>(p, gm, eb, tid);
                 group_sync<T>(g);
@@ -1329,8 +1330,7 @@ __global__ void __launch_bounds__(max_threads(W, BP4, NP), W == 0 ? 1 : 0) decod
                 const int valid = p.ell - 32 * wd;
                 const uint32_t full = valid >= 32 ? 0xffffffffu : (valid > 0 ? (1u << valid) - 1u : 0u);
                 const uint32_t x = (hd0 & 1u) ? full : 0u, z = (hd0 >> 1) ? full : 0u;
-                gm.bits[kXL * nw1 + wd] = x; gm.bits[kZL * nw1 + wd] = z;
-                gm.bits[kXR * nw1 + wd] = x; gm.bits[kZR * nw1 + wd] = z;
+                store_bits4(gm.bits, wd, x, z, x, z);
             }
         } else {
             if (p.sample) {
