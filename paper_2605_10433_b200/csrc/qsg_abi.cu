@@ -378,8 +378,11 @@ int launch_cfg(qsg_graph *g, bool bp4, bool add, bool lean, void *fn, qsg::Launc
     int gmax = std::min(640, fa.maxThreadsPerBlock) / T;
     int cap_sm = 1 << 30;         // QSG_MAX_FRAMES_PER_SM: tuning/diagnostics only
     if (const char *env = std::getenv("QSG_MAX_FRAMES_PER_SM")) cap_sm = std::max(1, std::atoi(env));
+    int force_g = 0;              // QSG_GROUPS: tuning/diagnostics only
+    if (const char *env = std::getenv("QSG_GROUPS")) force_g = std::atoi(env);
     qsg::LaunchCfg best;
     for (int G = 1; G <= gmax; ++G) {
+        if (force_g > 0 && G != std::min(force_g, gmax)) continue;
         const size_t smem = g->tab_bytes + (size_t)G * g->group_bytes;
         if (smem > (size_t)max_smem) break;
         int nb = 0;
@@ -387,13 +390,18 @@ int launch_cfg(qsg_graph *g, bool bp4, bool add, bool lean, void *fn, qsg::Launc
         nb = std::min(nb, cap_sm / G);
         if (nb * G > best.ctas_per_sm * best.groups) {
             best.groups = G; best.ctas_per_sm = nb; best.smem = smem; best.ok = nb > 0;
+            best.big_groups = 0;
+        } else if (nb > 0 && nb * G == best.ctas_per_sm * best.groups) {
+            best.big_groups = G; best.big_ctas_per_sm = nb; best.big_smem = smem;  // same frames, larger CTAs
         }
     }
     if (!best.ok) return fail(QSG_EUNSUPPORTED, "graph does not fit in shared memory");
     if (std::getenv("QSG_VERBOSE"))  // diagnostics
-        std::fprintf(stderr, "qsg launch_cfg: kind %d T %d bp4 %d regs %d groups %d ctas/SM %d smem %zu (group %u, tab %u)\n",
+        std::fprintf(stderr, "qsg launch_cfg: kind %d T %d bp4 %d regs %d groups %d ctas/SM %d smem %zu (group %u, tab %u); "
+                     "full batches: groups %d ctas/SM %d\n",
                      g->kind, T, (int)bp4, fa.numRegs, best.groups, best.ctas_per_sm, best.smem, g->group_bytes,
-                     g->tab_bytes);
+                     g->tab_bytes, best.big_groups ? best.big_groups : best.groups,
+                     best.big_groups ? best.big_ctas_per_sm : best.ctas_per_sm);
     c = best;
     *out = best;
     return QSG_OK;
@@ -425,6 +433,13 @@ int launch_decode(qsg_graph *g, const qsg_decoder_cfg *cfg, qsg::KParams &p, cud
     int rc = launch_cfg(g, bp4, add, lean, fn, &lc);
     if (rc) return rc;
     if (p.count == 0) return QSG_OK;
+    // a batch that fills every SM runs in the largest CTAs holding the same
+    // number of frames per SM (+1-1.5% measured: one table copy per SM, an
+    // even spread of the warps over the schedulers); smaller batches keep
+    // the small CTAs, which reach more SMs
+    if (lc.big_groups > 0 && p.count >= (int64_t)lc.big_groups * lc.big_ctas_per_sm * g->num_sms) {
+        lc.groups = lc.big_groups; lc.ctas_per_sm = lc.big_ctas_per_sm; lc.smem = lc.big_smem;
+    }
     const int64_t want = (p.count + lc.groups - 1) / lc.groups;
     const int grid = (int)std::min<int64_t>(want, (int64_t)lc.ctas_per_sm * g->num_sms);
     unsigned long long *queue = nullptr;

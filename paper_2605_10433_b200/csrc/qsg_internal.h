@@ -33,6 +33,11 @@ struct LaunchCfg {
     int ctas_per_sm = 0;
     size_t smem = 0;
     bool ok = false;
+    // the same number of frames per SM in the fewest, largest CTAs (used when
+    // the batch fills every SM: one table copy per SM, warps spread evenly
+    // over the four schedulers); 0 when it is the configuration above
+    int big_groups = 0, big_ctas_per_sm = 0;
+    size_t big_smem = 0;
 };
 
 }  // namespace qsg
