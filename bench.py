@@ -251,6 +251,14 @@ def run_ours(args, rank, world, local_rank):
             step_ms.append(s0.elapsed_time(s1))
             for k in range(len(points)):
                 launch_ms[k][0] += ev[k][0].elapsed_time(ev[k][1])
+        # a timed region shorter than nvidia-smi's start-up plus one sampling
+        # period (reduced test workloads) would leave no clock sample: keep
+        # the same load running, untimed, until the first sample arrives
+        # (single rank only: step() holds a collective when world > 1)
+        t_wait = time.perf_counter()
+        while world == 1 and not sampler.lines and sampler.proc and time.perf_counter() - t_wait < 5.0:
+            step()
+            torch.cuda.synchronize()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
